@@ -1,0 +1,38 @@
+# Builds every native artefact in-tree (they travel to the GPU box with the
+# gpurun snapshot; .so files are git-ignored).
+#   lib/libaspamg_host.so : CPU setup + generator (C++20, OpenMP)
+#   lib/libaspamg_gpu.so  : sm_100a CUDA solve path + C-ABI (include/aspamg_gpu.h)
+#   oracle/liboracle.so   : CPU oracle (test infrastructure only)
+#   oracle/_ref/*.so      : the reference's own sparse kernels (only when /root/reference exists)
+PKG      := paper_1902_01715_b200
+LIB      := $(PKG)/lib
+HOSTSRC  := $(wildcard $(PKG)/csrc/host/*.cpp)
+HOSTHDR  := $(wildcard $(PKG)/csrc/host/*.hpp) include/aspamg_host.h
+GPUSRC   := $(wildcard $(PKG)/csrc/gpu/*.cu)
+GPUHDR   := $(wildcard $(PKG)/csrc/gpu/*.cuh) include/aspamg_gpu.h
+NVCC     := /usr/local/cuda/bin/nvcc
+# /usr/bin/g++ explicitly: the image exports CXX=/opt/gcc/bin/g++, which lacks libgomp
+CXX      := /usr/bin/g++
+# Portable x86-64 baseline: the GPU box's host CPU is not this container's.
+CXXFLAGS := -std=c++20 -O3 -march=x86-64-v2 -ffp-contract=off -fPIC -fopenmp -Wall -Wextra
+NVFLAGS  := -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a \
+            -ccbin /usr/bin/g++ -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+
+all: $(LIB)/libaspamg_host.so $(LIB)/libaspamg_gpu.so oracle
+
+$(LIB)/libaspamg_host.so: $(HOSTSRC) $(HOSTHDR)
+	@mkdir -p $(LIB)
+	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOSTSRC)
+
+$(LIB)/libaspamg_gpu.so: $(GPUSRC) $(GPUHDR)
+	@mkdir -p $(LIB)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPUSRC) 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -f $(LIB)/*.so $(LIB)/ptxas.log
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

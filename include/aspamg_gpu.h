@@ -1,0 +1,113 @@
+/* aspamg_gpu.h — C-ABI of the B200 (sm_100a) solve phase: PCG with one
+ * aSP-AMG V(nu1,nu2)-cycle per iteration, every per-iteration operation in
+ * hand-written CUDA (lib/libaspamg_gpu.so). No cuSPARSE/cuBLAS, no CPU
+ * fallback: without a CUDA device every call fails with status 5.
+ *
+ * Reference interfaces each entry point replaces (the reference declares the
+ * path in C++ and SPEC text; hierarchy.cpp / krylov.cpp / fsai.cpp are
+ * missing, core/CMakeLists.txt:9-14):
+ *   aspamg_gpu_upload_level   <- Level {A_k, FsaiSmoother{G, omega}, P_k}
+ *                                SPEC.md:422-425, fsai.hpp:44-53; CSR exactly
+ *                                as SparseMatrix (sparse_matrix.hpp:27-33);
+ *                                G' and P' explicit (transpose, sparse_matrix.cpp:168-189)
+ *   aspamg_gpu_upload_coarse  <- Hierarchy::coarse_factor (dense Cholesky),
+ *                                SPEC.md:430-433,478
+ *   aspamg_gpu_vcycle         <- vcycle_apply(h, y)  SPEC.md:445-453, Alg. 2
+ *   aspamg_gpu_smooth         <- apply_smoothing_step(s, A, b, x) fsai.hpp:78-80
+ *   aspamg_gpu_spmv           <- spmv(A, x) sparse_matrix.hpp:61-63 (on any uploaded operand)
+ *   aspamg_gpu_pcg            <- pcg(A, b, precond, rel_tol, max_it, x0) SPEC.md:504-512,
+ *                                A = finest A_0, precond = the uploaded V-cycle;
+ *                                SolveReport fields n_it / residual_history /
+ *                                converged
+ *
+ * Status codes: 0 OK, 1 dimension mismatch (DimensionError),
+ * 2 not SPD: p'Ap <= 0 (NotSpdError), 3 numerical (NumericalError), 4 config
+ * (ConfigError), 5 CUDA/runtime, 6 not converged (converged = 0, x valid).
+ * Ownership: host buffers are borrowed for the duration of a call; all device
+ * memory belongs to the context. Threading: one context = one CUDA stream,
+ * calls on one context must be serialized; distinct contexts may run
+ * concurrently.
+ */
+#ifndef ASPAMG_GPU_H
+#define ASPAMG_GPU_H
+
+#include <stdint.h>
+
+#include "aspamg_csr.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct aspamg_gpu_ctx aspamg_gpu_ctx;
+
+typedef struct aspamg_gpu_level_stats {
+    int64_t n;
+    int32_t a_format;     /* 0 CSR, 1 exact 3x3 BSR */
+    int64_t a_nnz, a_nnzb;
+    double a_fill;        /* stored values / true nnz (1.0 = exact) */
+    int64_t g_nnz, p_nnz;
+    double omega;
+    double alg_bytes_A, alg_bytes_G, alg_bytes_Gt, alg_bytes_P, alg_bytes_Pt; /* one product each */
+    double device_bytes;
+} aspamg_gpu_level_stats;
+
+typedef struct aspamg_gpu_kernel_time {
+    char name[48];
+    int32_t level;
+    double ms;
+    double alg_bytes;
+} aspamg_gpu_kernel_time;
+
+const char* aspamg_gpu_last_error(const aspamg_gpu_ctx* ctx); /* ctx may be NULL (thread's last) */
+int aspamg_gpu_device_count(int* n);
+int aspamg_gpu_ctx_create(int device, aspamg_gpu_ctx** out);
+int aspamg_gpu_ctx_destroy(aspamg_gpu_ctx* ctx);
+/* keys: "bsr" (1 auto, 0 never), "device_loop" (1 CUDA-graph while-loop, 0 host loop),
+ *       "stream_bytes" (matrices above this many bytes use evict-first loads) */
+int aspamg_gpu_set_option(aspamg_gpu_ctx* ctx, const char* key, int64_t value);
+int aspamg_gpu_set_cycle(aspamg_gpu_ctx* ctx, int64_t nu1, int64_t nu2);
+/* Levels 0..L-2 carry A, G, G', P, P' and omega; the coarsest level L-1 carries
+ * A only (G..Pt may be NULL or empty). Levels must be uploaded in order. */
+int aspamg_gpu_upload_level(aspamg_gpu_ctx* ctx, int64_t level, const aspamg_csr_view* A,
+                            const aspamg_csr_view* G, const aspamg_csr_view* Gt,
+                            const aspamg_csr_view* P, const aspamg_csr_view* Pt, double omega);
+int aspamg_gpu_upload_coarse(aspamg_gpu_ctx* ctx, int64_t n_c, const double* L_colmajor);
+int aspamg_gpu_finalize(aspamg_gpu_ctx* ctx);
+
+int aspamg_gpu_num_levels(aspamg_gpu_ctx* ctx, int64_t* n);
+int aspamg_gpu_level_info(aspamg_gpu_ctx* ctx, int64_t level, aspamg_gpu_level_stats* out);
+
+/* host buffers */
+int aspamg_gpu_vcycle(aspamg_gpu_ctx* ctx, const double* y, double* z);
+int aspamg_gpu_spmv(aspamg_gpu_ctx* ctx, int64_t level, int which /*0 A,1 G,2 G',3 P,4 P'*/,
+                    const double* x, double* y);
+int aspamg_gpu_smooth(aspamg_gpu_ctx* ctx, int64_t level, const double* b, const double* x, double* out);
+int aspamg_gpu_coarse_solve(aspamg_gpu_ctx* ctx, const double* y, double* z);
+int aspamg_gpu_pcg(aspamg_gpu_ctx* ctx, const double* b, const double* x0_or_null, double rel_tol,
+                   int64_t max_it, double* x, double* history, int64_t* n_it, int* converged,
+                   double* true_rel_res);
+/* device buffers (b, x0, x on the context's device); history is a host buffer */
+int aspamg_gpu_vcycle_device(aspamg_gpu_ctx* ctx, const double* y_dev, double* z_dev);
+int aspamg_gpu_pcg_device(aspamg_gpu_ctx* ctx, const double* b_dev, const double* x0_dev_or_null,
+                          double rel_tol, int64_t max_it, double* x_dev, double* history,
+                          int64_t* n_it, int* converged, double* true_rel_res);
+
+/* measurement helpers */
+int aspamg_gpu_last_solve_ms(aspamg_gpu_ctx* ctx, double* ms);      /* device time of the last pcg */
+int aspamg_gpu_launch_count(aspamg_gpu_ctx* ctx, int64_t* n);       /* kernels launched by the last pcg */
+int aspamg_gpu_profile_iteration(aspamg_gpu_ctx* ctx, aspamg_gpu_kernel_time* out, int cap, int* count);
+int aspamg_gpu_time_kernel(aspamg_gpu_ctx* ctx, const char* name, int64_t level, int reps,
+                           double* avg_ms, double* alg_bytes);
+int aspamg_gpu_stream(aspamg_gpu_ctx* ctx, void** stream);
+int aspamg_gpu_alloc_pinned(int64_t bytes, void** out);
+int aspamg_gpu_free_pinned(void* p);
+int aspamg_gpu_alloc_device(aspamg_gpu_ctx* ctx, int64_t bytes, void** out);
+int aspamg_gpu_free_device(aspamg_gpu_ctx* ctx, void* p);
+int aspamg_gpu_memcpy(aspamg_gpu_ctx* ctx, void* dst, const void* src, int64_t bytes); /* any direction, synchronous */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ASPAMG_GPU_H */

@@ -1,0 +1,1036 @@
+// Device context, hierarchy upload, V-cycle / PCG orchestration (CUDA graph
+// with a device-side while loop) and the C-ABI of include/aspamg_gpu.h.
+//
+// Orchestration restates, on the device:
+//   vcycle_apply  SPEC.md:445-453 / Alg. 2 PAPER.md:287-306 (s = 0 start, so the
+//                 first pre-smoothing step is s = w G'(G y) exactly)
+//   pcg           SPEC.md:504-512 (x0 = 0 default, ||r|| <= tol ||b||, not-SPD on
+//                 p'Ap <= 0, true-residual recheck x10)
+// The iteration is rotated so the convergence test is the last kernel of the
+// loop body: body = [V-cycle(r)->z (+ r.z -> beta), p = z + beta p,
+// q = K p (+ p.q -> alpha), x += alpha p, r -= alpha q (+ r.r -> history,
+// test -> graph condition)]. This is the reference's order of operations.
+#include "../../../include/aspamg_gpu.h"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+using namespace aspamg_gpu;
+
+namespace {
+
+thread_local std::string g_last_err;
+
+struct Op {
+    std::string name;
+    int level;
+    double bytes;  // algorithmic bytes (compulsory traffic)
+    std::function<void(cudaStream_t)> fn;
+};
+
+struct GLevel {
+    int n = 0;
+    DMat A, G, Gt, P, Pt;
+    double omega = 1.0;
+    bool has_smoother = false;
+    double* y = nullptr;  // input (levels > 0)
+    double* z = nullptr;  // output == s accumulator (levels > 0)
+    double* r = nullptr;
+    double* t = nullptr;
+    long long a_nnz = 0;
+};
+
+struct Site {  // one deterministic reduction site
+    double* partials = nullptr;
+    unsigned* counter = nullptr;
+};
+
+}  // namespace
+
+struct aspamg_gpu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    std::vector<GLevel> lv;
+    int nu1 = 1, nu2 = 1;
+    // coarsest factor
+    int n_c = 0;
+    double *Lrm = nullptr, *Lcm = nullptr, *Dinv_f = nullptr, *Dinv_b = nullptr;
+    bool coarse_uploaded = false;
+    bool finalized = false;
+    // options
+    int opt_bsr = 1, opt_device_loop = 1;
+    long long opt_stream_bytes = 48ll << 20;
+    // PCG state and vectors
+    PcgState* st = nullptr;       // device
+    PcgState* st_host = nullptr;  // pinned
+    int* zero_flag = nullptr;     // device int 0 (done pointer for standalone calls)
+    double *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+    double* hist = nullptr;
+    long long hist_cap = 0;
+    double *vy = nullptr, *vz = nullptr;  // standalone V-cycle in/out
+    std::vector<void*> allocs;
+    std::vector<Site> sites;
+    // op lists + graphs
+    std::vector<Op> body, vc_ops, init0, init1, post;
+    cudaGraphExec_t pcg_exec = nullptr, body_exec = nullptr, vc_exec = nullptr;
+    cudaGraph_t pcg_graph = nullptr, body_graph = nullptr, vc_graph = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_ms = 0.0;
+    long long last_launches = 0;
+    size_t device_bytes = 0;
+};
+
+namespace {
+
+struct CudaFail {
+    std::string msg;
+};
+
+#define CK(call)                                                                                 \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            throw CudaFail{std::string(#call) + ": " + cudaGetErrorString(e_)};                  \
+    } while (0)
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+template <class F>
+int guard(aspamg_gpu_ctx* c, F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const Fail& e) {
+        if (c) c->err = e.msg;
+        g_last_err = e.msg;
+        return e.code;
+    } catch (const CudaFail& e) {
+        if (c) c->err = e.msg;
+        g_last_err = e.msg;
+        return 5;
+    } catch (const std::bad_alloc&) {
+        if (c) c->err = "out of host memory";
+        g_last_err = "out of host memory";
+        return 5;
+    } catch (const std::exception& e) {
+        if (c) c->err = e.what();
+        g_last_err = e.what();
+        return 5;
+    }
+}
+
+template <class T>
+T* dalloc(aspamg_gpu_ctx* c, size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    c->allocs.push_back(p);
+    c->device_bytes += count * sizeof(T);
+    return static_cast<T*>(p);
+}
+
+Red make_red(aspamg_gpu_ctx* c, int grid, int fin, double* out = nullptr) {
+    Site s;
+    s.partials = dalloc<double>(c, 2 * (size_t)std::max(grid, 1));
+    s.counter = dalloc<unsigned>(c, 1);
+    CK(cudaMemset(s.counter, 0, sizeof(unsigned)));
+    c->sites.push_back(s);
+    Red r;
+    r.partials = s.partials;
+    r.counter = s.counter;
+    r.fin = fin;
+    r.out = out;
+    r.st = c->st;
+    return r;
+}
+
+// ----------------------------------------------------------- format choice
+bool exact_bsr3(const aspamg_csr_view& v) {
+    if (v.n_rows % 3 || v.n_cols % 3 || v.n_rows == 0) return false;
+    const int64_t* rp = v.row_offsets;
+    const int64_t* ci = v.col_indices;
+    for (int64_t br = 0; br < v.n_rows / 3; ++br) {
+        const int64_t r0 = 3 * br;
+        const int64_t len = rp[r0 + 1] - rp[r0];
+        if (len % 3) return false;
+        for (int k = 1; k < 3; ++k)
+            if (rp[r0 + k + 1] - rp[r0 + k] != len) return false;
+        for (int64_t t = 0; t < len; t += 3) {
+            const int64_t c0 = ci[rp[r0] + t];
+            if (c0 % 3) return false;
+            for (int k = 0; k < 3; ++k)
+                for (int cc = 0; cc < 3; ++cc)
+                    if (ci[rp[r0 + k] + t + cc] != c0 + cc) return false;
+        }
+    }
+    return true;
+}
+
+void check_view(const aspamg_csr_view* v, const char* what) {
+    if (!v) throw Fail{1, std::string(what) + ": null matrix"};
+    if (v->n_rows < 0 || v->n_cols < 0) throw Fail{1, std::string(what) + ": negative size"};
+    if (v->n_rows > 0 && !v->row_offsets) throw Fail{1, std::string(what) + ": null row_offsets"};
+    if (v->n_rows > 0 && v->row_offsets[v->n_rows] != v->nnz) throw Fail{1, std::string(what) + ": nnz mismatch"};
+    if (v->nnz >= (1ll << 31) || v->n_rows >= (1ll << 31) || v->n_cols >= (1ll << 31))
+        throw Fail{4, std::string(what) + ": exceeds int32 device indexing"};
+    for (int64_t k = 0; k < v->nnz; ++k)
+        if (v->col_indices[k] < 0 || v->col_indices[k] >= v->n_cols)
+            throw Fail{1, std::string(what) + ": column index out of range"};
+}
+
+int group_for(double mean) {
+    int g = 1;
+    while (g < 32 && 2.0 * g <= mean) g *= 2;
+    return g;
+}
+
+DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
+    DMat M;
+    const long long nnz = v.nnz;
+    const bool bsr = allow_bsr && c->opt_bsr && exact_bsr3(v);
+    if (bsr) {
+        M.fmt = 1;
+        DBsr3& B = M.bsr;
+        B.nb = (int)(v.n_rows / 3);
+        B.nbc = (int)(v.n_cols / 3);
+        B.nnzb = nnz / 9;
+        std::vector<int> rp(B.nb + 1), ci((size_t)B.nnzb);
+        std::vector<double> val((size_t)nnz);
+        for (int br = 0; br < B.nb; ++br) {
+            const int64_t r0 = 3 * (int64_t)br;
+            const int64_t len = v.row_offsets[r0 + 1] - v.row_offsets[r0];
+            const int64_t b0 = v.row_offsets[r0] / 9;  // 9 values per block, block rows consecutive
+            rp[br] = (int)b0;
+            for (int64_t t = 0; t < len / 3; ++t) {
+                ci[(size_t)(b0 + t)] = (int)(v.col_indices[v.row_offsets[r0] + 3 * t] / 3);
+                for (int r = 0; r < 3; ++r)
+                    for (int cc = 0; cc < 3; ++cc)
+                        val[(size_t)(9 * (b0 + t) + 3 * r + cc)] = v.values[v.row_offsets[r0 + r] + 3 * t + cc];
+            }
+        }
+        rp[B.nb] = (int)B.nnzb;
+        B.rp = dalloc<int>(c, rp.size());
+        B.ci = dalloc<int>(c, ci.size());
+        B.v = dalloc<double>(c, val.size());
+        CK(cudaMemcpy(B.rp, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(B.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(B.v, val.data(), val.size() * sizeof(double), cudaMemcpyHostToDevice));
+        B.stream = (long long)(76.0 * B.nnzb) > c->opt_stream_bytes;
+        return M;
+    }
+    M.fmt = 0;
+    DCsr& A = M.csr;
+    A.n_rows = (int)v.n_rows;
+    A.n_cols = (int)v.n_cols;
+    A.nnz = nnz;
+    std::vector<int> rp((size_t)v.n_rows + 1), ci((size_t)nnz);
+    for (int64_t i = 0; i <= v.n_rows; ++i) rp[(size_t)i] = (int)(v.n_rows ? v.row_offsets[i] : 0);
+    for (int64_t k = 0; k < nnz; ++k) ci[(size_t)k] = (int)v.col_indices[k];
+    A.rp = dalloc<int>(c, rp.size());
+    A.ci = dalloc<int>(c, ci.size());
+    A.v = dalloc<double>(c, (size_t)nnz);
+    CK(cudaMemcpy(A.rp, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (nnz) {
+        CK(cudaMemcpy(A.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(A.v, v.values, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    A.group = group_for(v.n_rows ? double(nnz) / double(v.n_rows) : 1.0);
+    A.stream = (long long)(12.0 * nnz) > c->opt_stream_bytes;
+    return M;
+}
+
+// Algorithmic bytes of one product y = M x: matrix arrays
+// once, x once, y once; padding never counted.
+double alg_bytes(const DMat& M) {
+    if (M.fmt == 1) {
+        const double nnzb = double(M.bsr.nnzb);
+        return 72.0 * nnzb + 4.0 * nnzb + 4.0 * (M.bsr.nb + 1) + 8.0 * M.cols() + 8.0 * M.rows();
+    }
+    const double nnz = double(M.csr.nnz);
+    return 8.0 * nnz + 4.0 * nnz + 4.0 * (M.csr.n_rows + 1) + 8.0 * M.cols() + 8.0 * M.rows();
+}
+
+std::string fmt_name(const DMat& M) { return M.fmt == 1 ? "bsr3" : "csr" + std::to_string(M.csr.group); }
+
+void add_spmv(aspamg_gpu_ctx* c, std::vector<Op>& ops, const std::string& name, int level, const DMat& M, Epi epi,
+              const double* x, double* y, const double* aux, double omega, const double* dotw, int fin,
+              double* out, const int* done) {
+    const int grid = spmv_grid(M);
+    Red red;
+    if (fin != FIN_NONE) red = make_red(c, grid, fin, out);
+    double bytes = alg_bytes(M);
+    if (aux) bytes += 8.0 * M.rows();
+    if (dotw) bytes += 8.0 * M.rows();
+    const DMat Mc = M;
+    ops.push_back({name + "." + fmt_name(M), level, bytes, [=](cudaStream_t s) {
+                       Launch L{grid, s};
+                       spmv(Mc, epi, x, y, aux, omega, dotw, red, done, L);
+                   }});
+}
+
+// V-cycle ops at level k: input y, output z (z doubles as the s accumulator).
+// dotw0/fin0: the dot fused into the last op that writes the level-0 output.
+void build_vcycle(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* y, double* z, const double* dotw0,
+                  int fin0, const int* done) {
+    const int L = (int)c->lv.size();
+    const bool top = k == 0;
+    if (k == L - 1) {  // coarsest: forward/backward solve
+        Red red;
+        if (top && fin0 != FIN_NONE) red = make_red(c, 1, fin0);
+        const int n = c->n_c;
+        const double *Lrm = c->Lrm, *Lcm = c->Lcm, *Df = c->Dinv_f, *Db = c->Dinv_b;
+        const double* dw = top ? dotw0 : nullptr;
+        const double bytes = 2.0 * (8.0 * double(n) * (n + 1) / 2 + 16.0 * n);
+        ops.push_back({"coarse_solve", k, bytes, [=](cudaStream_t s) {
+                           Launch Lc{1, s};
+                           coarse_solve(n, Lrm, Lcm, Df, Db, y, z, dw, red, done, Lc);
+                       }});
+        return;
+    }
+    GLevel& l = c->lv[(size_t)k];
+    const int n = l.n;
+    double* s = z;
+    const GLevel& nx = c->lv[(size_t)k + 1];
+    double* yc = nx.y;
+    double* zc = nx.z;
+    // pre-smoothing from s = 0
+    for (int it = 0; it < c->nu1; ++it) {
+        if (it == 0) {
+            add_spmv(c, ops, "smooth_G", k, l.G, EPI_PLAIN, y, l.t, nullptr, 1.0, nullptr, FIN_NONE, nullptr, done);
+            add_spmv(c, ops, "smooth_Gt", k, l.Gt, EPI_SCALE, l.t, s, nullptr, l.omega, nullptr, FIN_NONE, nullptr, done);
+        } else {
+            add_spmv(c, ops, "resid_A", k, l.A, EPI_RESID, s, l.r, y, 1.0, nullptr, FIN_NONE, nullptr, done);
+            add_spmv(c, ops, "smooth_G", k, l.G, EPI_PLAIN, l.r, l.t, nullptr, 1.0, nullptr, FIN_NONE, nullptr, done);
+            add_spmv(c, ops, "smooth_Gt", k, l.Gt, EPI_ADDSCALE, l.t, s, s, l.omega, nullptr, FIN_NONE, nullptr, done);
+        }
+    }
+    if (c->nu1 == 0) {
+        const int g = vec_grid(n);
+        ops.push_back({"zero", k, 8.0 * n, [=](cudaStream_t st) { fill_zero(n, s, done, Launch{g, st}); }});
+    }
+    // r = y - A s ; r_c = P' r
+    add_spmv(c, ops, "resid_A", k, l.A, EPI_RESID, s, l.r, y, 1.0, nullptr, FIN_NONE, nullptr, done);
+    add_spmv(c, ops, "restrict_Pt", k, l.Pt, EPI_PLAIN, l.r, yc, nullptr, 1.0, nullptr, FIN_NONE, nullptr, done);
+    build_vcycle(c, ops, k + 1, yc, zc, dotw0, fin0, done);
+    // s += P e_c
+    const bool last_is_prolong = c->nu2 == 0;
+    add_spmv(c, ops, "prolong_P", k, l.P, EPI_ADD, zc, s, s, 1.0, (top && last_is_prolong) ? dotw0 : nullptr,
+             (top && last_is_prolong) ? fin0 : FIN_NONE, nullptr, done);
+    for (int it = 0; it < c->nu2; ++it) {
+        const bool last = top && it == c->nu2 - 1;
+        add_spmv(c, ops, "resid_A", k, l.A, EPI_RESID, s, l.r, y, 1.0, nullptr, FIN_NONE, nullptr, done);
+        add_spmv(c, ops, "smooth_G", k, l.G, EPI_PLAIN, l.r, l.t, nullptr, 1.0, nullptr, FIN_NONE, nullptr, done);
+        add_spmv(c, ops, "smooth_Gt", k, l.Gt, EPI_ADDSCALE, l.t, s, s, l.omega, last ? dotw0 : nullptr,
+                 last ? fin0 : FIN_NONE, nullptr, done);
+    }
+}
+
+void run_ops(const std::vector<Op>& ops, cudaStream_t s) {
+    for (const auto& o : ops) o.fn(s);
+}
+
+void ensure_ready(aspamg_gpu_ctx* c) {
+    if (!c) throw Fail{4, "null context"};
+    if (!c->finalized) throw Fail{4, "context not finalized (upload levels + coarse factor, then finalize)"};
+}
+
+void build_graphs(aspamg_gpu_ctx* c) {
+    // standalone V-cycle graph
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    run_ops(c->vc_ops, c->stream);
+    CK(cudaStreamEndCapture(c->stream, &c->vc_graph));
+    CK(cudaGraphInstantiate(&c->vc_exec, c->vc_graph, 0));
+    // PCG body graph (host-loop fallback)
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    run_ops(c->body, c->stream);
+    CK(cudaStreamEndCapture(c->stream, &c->body_graph));
+    CK(cudaGraphInstantiate(&c->body_exec, c->body_graph, 0));
+}
+
+// Device-side loop: parent graph = WHILE(cond) { body }; the last kernel of the
+// body (pcg_xr) sets the condition from the convergence test.
+void build_device_loop(aspamg_gpu_ctx* c) {
+    CK(cudaGraphCreate(&c->pcg_graph, 0));
+    cudaGraphConditionalHandle handle;
+    CK(cudaGraphConditionalHandleCreate(&handle, c->pcg_graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, c->pcg_graph, nullptr, 0, &cp));
+    cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+    // rebuild the body op list with the condition handle wired into pcg_xr
+    const std::vector<Op>& body = c->body;
+    CK(cudaStreamBeginCaptureToGraph(c->stream, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    for (size_t i = 0; i + 1 < body.size(); ++i) body[i].fn(c->stream);
+    {
+        // pcg_xr with the conditional
+        const int n = c->lv[0].n;
+        const int g = vec_grid(n);
+        Red red = make_red(c, g, FIN_RR);
+        red.cond = handle;
+        red.use_cond = 1;
+        double *x = c->x, *r = c->r, *p = c->p, *q = c->q;
+        const int* done = &c->st->done;
+        pcg_xr(n, x, r, p, q, red, done, Launch{g, c->stream});
+    }
+    cudaGraph_t out;
+    CK(cudaStreamEndCapture(c->stream, &out));
+    CK(cudaGraphInstantiate(&c->pcg_exec, c->pcg_graph, 0));
+}
+
+void do_finalize(aspamg_gpu_ctx* c) {
+    if ((int)c->lv.size() < 1) throw Fail{4, "finalize: no levels uploaded"};
+    if (!c->coarse_uploaded) throw Fail{4, "finalize: coarse factor not uploaded"};
+    const int L = (int)c->lv.size();
+    if (c->lv.back().n != c->n_c) throw Fail{1, "finalize: coarse factor size does not match the last level"};
+    for (int k = 0; k + 1 < L; ++k) {
+        GLevel& l = c->lv[(size_t)k];
+        if (!l.has_smoother) throw Fail{4, "finalize: level " + std::to_string(k) + " lacks G/P"};
+        if (l.P.cols() != c->lv[(size_t)k + 1].n) throw Fail{1, "finalize: P columns != next level size"};
+    }
+    const int n0 = c->lv[0].n;
+    c->st = dalloc<PcgState>(c, 1);
+    CK(cudaMemset(c->st, 0, sizeof(PcgState)));
+    CK(cudaMallocHost(&c->st_host, sizeof(PcgState)));
+    c->zero_flag = dalloc<int>(c, 1);
+    CK(cudaMemset(c->zero_flag, 0, sizeof(int)));
+    c->b = dalloc<double>(c, n0);
+    c->x = dalloc<double>(c, n0);
+    c->r = dalloc<double>(c, n0);
+    c->z = dalloc<double>(c, n0);
+    c->p = dalloc<double>(c, n0);
+    c->q = dalloc<double>(c, n0);
+    c->vy = dalloc<double>(c, n0);
+    c->vz = dalloc<double>(c, n0);
+    for (int k = 0; k < L; ++k) {
+        GLevel& l = c->lv[(size_t)k];
+        if (k > 0) {
+            l.y = dalloc<double>(c, l.n);
+            l.z = dalloc<double>(c, l.n);
+        }
+        if (k + 1 < L) {
+            l.r = dalloc<double>(c, l.n);
+            l.t = dalloc<double>(c, l.n);
+        }
+    }
+    const int* done = &c->st->done;
+    // standalone V-cycle: vy -> vz
+    build_vcycle(c, c->vc_ops, 0, c->vy, c->vz, nullptr, FIN_NONE, c->zero_flag);
+    // PCG loop body
+    build_vcycle(c, c->body, 0, c->r, c->z, c->r, FIN_RZ, done);
+    {
+        const int g = vec_grid(n0);
+        double *z = c->z, *p = c->p;
+        const PcgState* st = c->st;
+        c->body.push_back({"pcg_p", 0, 24.0 * n0, [=](cudaStream_t s) { pcg_p(n0, z, p, st, done, Launch{g, s}); }});
+    }
+    add_spmv(c, c->body, "pcg_Kp", 0, c->lv[0].A, EPI_PLAIN, c->p, c->q, nullptr, 1.0, c->p, FIN_PQ, nullptr, done);
+    {
+        const int g = vec_grid(n0);
+        Red red = make_red(c, g, FIN_RR);
+        double *x = c->x, *r = c->r, *p = c->p, *q = c->q;
+        c->body.push_back({"pcg_xr", 0, 48.0 * n0, [=](cudaStream_t s) { pcg_xr(n0, x, r, p, q, red, done, Launch{g, s}); }});
+    }
+    // init: x0 given -> r = b - A x ; then dots b.b, r.r
+    add_spmv(c, c->init1, "init_resid", 0, c->lv[0].A, EPI_RESID, c->x, c->r, c->b, 1.0, nullptr, FIN_NONE, nullptr,
+             nullptr);
+    {
+        const int g = vec_grid(n0);
+        Red red = make_red(c, g, FIN_INIT);
+        double *b = c->b, *r = c->r;
+        c->init0.push_back({"init_dots", 0, 16.0 * n0, [=](cudaStream_t s) { pcg_init_dots(n0, b, r, red, Launch{g, s}); }});
+    }
+    // post: true residual q = b - A x, ||q||^2 -> st->trr2
+    add_spmv(c, c->post, "true_resid", 0, c->lv[0].A, EPI_RESID, c->x, c->q, c->b, 1.0, c->q, FIN_STORE,
+             &c->st->trr2, nullptr);
+    build_graphs(c);
+    if (c->opt_device_loop) {
+        try {
+            build_device_loop(c);
+        } catch (const CudaFail& e) {
+            std::fprintf(stderr, "aspamg_gpu: device-side loop unavailable (%s); using host loop\n", e.msg.c_str());
+            cudaGetLastError();
+            c->opt_device_loop = 0;
+        }
+    }
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    CK(cudaStreamSynchronize(c->stream));
+    c->finalized = true;
+}
+
+// Core device PCG: b, x0 already in c->b / c->x (if has_x0). Returns status.
+int run_pcg(aspamg_gpu_ctx* c, bool has_x0, double rel_tol, long long max_it, long long* n_it, int* converged,
+            double* trr) {
+    if (!(rel_tol >= 0.0)) throw Fail{4, "pcg: rel_tol must be >= 0"};
+    if (max_it < 0) throw Fail{4, "pcg: max_it must be >= 0"};
+    const int n0 = c->lv[0].n;
+    if (max_it + 1 > c->hist_cap) {
+        if (c->hist) cudaFree(c->hist);
+        c->hist_cap = std::max<long long>(max_it + 1, 1024);
+        CK(cudaMalloc(&c->hist, (size_t)c->hist_cap * sizeof(double)));
+    }
+    PcgState h = {};
+    h.tol = rel_tol;
+    h.max_it = max_it;
+    h.history = c->hist;
+    *c->st_host = h;
+    cudaStream_t s = c->stream;
+    long long launches = 0;
+    CK(cudaEventRecord(c->ev0, s));
+    CK(cudaMemcpyAsync(c->st, c->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+    if (has_x0) {
+        run_ops(c->init1, s);
+        launches += (long long)c->init1.size();
+    } else {
+        CK(cudaMemsetAsync(c->x, 0, (size_t)n0 * sizeof(double), s));
+        CK(cudaMemcpyAsync(c->r, c->b, (size_t)n0 * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    run_ops(c->init0, s);
+    launches += (long long)c->init0.size();
+    if (c->opt_device_loop && c->pcg_exec) {
+        CK(cudaGraphLaunch(c->pcg_exec, s));
+    } else {
+        // host loop: launch the body graph in batches, poll the done flag
+        long long it = 0;
+        CK(cudaMemcpyAsync(c->st_host, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        while (!c->st_host->done && it < max_it) {
+            const long long batch = std::min<long long>(4, max_it - it);
+            for (long long j = 0; j < batch; ++j) CK(cudaGraphLaunch(c->body_exec, s));
+            it += batch;
+            CK(cudaMemcpyAsync(c->st_host, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+    }
+    CK(cudaEventRecord(c->ev1, s));
+    run_ops(c->post, s);
+    launches += (long long)c->post.size();
+    CK(cudaMemcpyAsync(c->st_host, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->last_ms = ms;
+    const PcgState& st = *c->st_host;
+    // kernels that ran: every body op per iteration (plus the final body when already converged)
+    launches += (long long)c->body.size() * std::max<long long>(st.k, st.max_it > 0 ? 1 : 0);
+    c->last_launches = launches;
+    *n_it = st.k;
+    *converged = st.converged;
+    if (st.bnorm == 0.0) {
+        CK(cudaMemsetAsync(c->x, 0, (size_t)n0 * sizeof(double), s));
+        CK(cudaStreamSynchronize(s));
+        *trr = 0.0;
+        *converged = 1;
+        return 0;
+    }
+    *trr = std::sqrt(st.trr2) / st.bnorm;
+    if (*converged && !(*trr <= 10.0 * rel_tol)) *converged = 0;
+    if (st.notspd) throw Fail{2, "pcg: operator not SPD (p'Ap <= 0)"};
+    return *converged ? 0 : 6;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* aspamg_gpu_last_error(const aspamg_gpu_ctx* c) { return c ? c->err.c_str() : g_last_err.c_str(); }
+
+int aspamg_gpu_device_count(int* n) {
+    return guard(nullptr, [&] {
+        int d = 0;
+        cudaError_t e = cudaGetDeviceCount(&d);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            d = 0;
+        }
+        *n = d;
+    });
+}
+
+int aspamg_gpu_ctx_create(int device, aspamg_gpu_ctx** out) {
+    return guard(nullptr, [&] {
+        int nd = 0;
+        if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0) {
+            cudaGetLastError();
+            throw Fail{5, "no CUDA device: the B200 solve path has no CPU fallback"};
+        }
+        if (device < 0 || device >= nd) throw Fail{4, "invalid device index"};
+        CK(cudaSetDevice(device));
+        auto* c = new aspamg_gpu_ctx;
+        c->device = device;
+        cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete c;
+            throw CudaFail{std::string("cudaStreamCreate: ") + cudaGetErrorString(e)};
+        }
+        *out = c;
+    });
+}
+
+int aspamg_gpu_ctx_destroy(aspamg_gpu_ctx* c) {
+    if (!c) return 0;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
+    if (c->body_exec) cudaGraphExecDestroy(c->body_exec);
+    if (c->vc_exec) cudaGraphExecDestroy(c->vc_exec);
+    if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
+    if (c->body_graph) cudaGraphDestroy(c->body_graph);
+    if (c->vc_graph) cudaGraphDestroy(c->vc_graph);
+    for (void* p : c->allocs) cudaFree(p);
+    if (c->hist) cudaFree(c->hist);
+    if (c->st_host) cudaFreeHost(c->st_host);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return 0;
+}
+
+int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
+    return guard(c, [&] {
+        if (!c || !key) throw Fail{4, "set_option: null argument"};
+        if (c->finalized) throw Fail{4, "set_option: context already finalized"};
+        const std::string k(key);
+        if (k == "bsr") c->opt_bsr = (int)value;
+        else if (k == "device_loop") c->opt_device_loop = (int)value;
+        else if (k == "stream_bytes") c->opt_stream_bytes = value;
+        else throw Fail{4, "set_option: unknown key " + k};
+    });
+}
+
+int aspamg_gpu_set_cycle(aspamg_gpu_ctx* c, int64_t nu1, int64_t nu2) {
+    return guard(c, [&] {
+        if (!c) throw Fail{4, "null context"};
+        if (c->finalized) throw Fail{4, "set_cycle: context already finalized"};
+        if (nu1 < 0 || nu2 < 0 || nu1 + nu2 < 1 || nu1 > 16 || nu2 > 16)
+            throw Fail{4, "set_cycle: need nu1, nu2 >= 0, nu1 + nu2 >= 1"};
+        c->nu1 = (int)nu1;
+        c->nu2 = (int)nu2;
+    });
+}
+
+int aspamg_gpu_upload_level(aspamg_gpu_ctx* c, int64_t level, const aspamg_csr_view* A, const aspamg_csr_view* G,
+                            const aspamg_csr_view* Gt, const aspamg_csr_view* P, const aspamg_csr_view* Pt,
+                            double omega) {
+    return guard(c, [&] {
+        if (!c) throw Fail{4, "null context"};
+        if (c->finalized) throw Fail{4, "upload_level: context already finalized"};
+        if (level != (int64_t)c->lv.size()) throw Fail{4, "upload_level: levels must be uploaded in order"};
+        if (level >= 32) throw Fail{4, "upload_level: too many levels"};
+        CK(cudaSetDevice(c->device));
+        check_view(A, "A");
+        if (A->n_rows != A->n_cols) throw Fail{1, "upload_level: A must be square"};
+        if (level > 0) {
+            const GLevel& prev = c->lv.back();
+            if (prev.P.cols() != A->n_rows) throw Fail{1, "upload_level: A size != previous P columns"};
+        }
+        GLevel l;
+        l.n = (int)A->n_rows;
+        l.a_nnz = A->nnz;
+        l.A = upload_mat(c, *A, true);
+        const bool has = G && G->n_rows > 0;
+        if (has) {
+            check_view(G, "G"); check_view(Gt, "Gt"); check_view(P, "P"); check_view(Pt, "Pt");
+            if (G->n_rows != l.n || G->n_cols != l.n || Gt->n_rows != l.n || Gt->n_cols != l.n)
+                throw Fail{1, "upload_level: G/G' must be n x n"};
+            if (P->n_rows != l.n || Pt->n_cols != l.n || Pt->n_rows != P->n_cols)
+                throw Fail{1, "upload_level: P must be n x n_c and P' n_c x n"};
+            if (!(omega > 0.0) || !(omega <= 1.0)) throw Fail{4, "upload_level: omega must be in (0, 1]"};
+            l.G = upload_mat(c, *G, false);
+            l.Gt = upload_mat(c, *Gt, false);
+            l.P = upload_mat(c, *P, false);
+            l.Pt = upload_mat(c, *Pt, false);
+            l.omega = omega;
+            l.has_smoother = true;
+        }
+        c->lv.push_back(l);
+    });
+}
+
+int aspamg_gpu_upload_coarse(aspamg_gpu_ctx* c, int64_t n_c, const double* Lc) {
+    return guard(c, [&] {
+        if (!c) throw Fail{4, "null context"};
+        if (c->finalized) throw Fail{4, "upload_coarse: context already finalized"};
+        if (n_c < 1 || n_c > 20000) throw Fail{1, "upload_coarse: n_c out of range"};
+        if (!Lc) throw Fail{1, "upload_coarse: null factor"};
+        CK(cudaSetDevice(c->device));
+        const int n = (int)n_c;
+        std::vector<double> rm((size_t)n * n, 0.0), cm((size_t)n * n, 0.0);
+        for (int j = 0; j < n; ++j)
+            for (int i = j; i < n; ++i) {
+                const double v = Lc[(size_t)i + (size_t)j * n];
+                rm[(size_t)i * n + j] = v;  // row-major L
+                cm[(size_t)i + (size_t)j * n] = v;  // column-major L == row-major L'
+            }
+        for (int i = 0; i < n; ++i)
+            if (!(rm[(size_t)i * n + i] > 0.0)) throw Fail{3, "upload_coarse: non-positive diagonal in factor"};
+        // inverted 32x32 diagonal blocks (lower for L, upper for L')
+        const int nb = (n + 31) / 32;
+        std::vector<double> df((size_t)nb * 1024, 0.0), db((size_t)nb * 1024, 0.0);
+        for (int b = 0; b < nb; ++b) {
+            const int j0 = 32 * b, bs = std::min(32, n - j0);
+            double inv[32][32] = {};
+            for (int col = 0; col < bs; ++col) {  // solve L_b x = e_col
+                double xv[32] = {};
+                for (int i = 0; i < bs; ++i) {
+                    double s = (i == col) ? 1.0 : 0.0;
+                    for (int k = 0; k < i; ++k) s -= rm[(size_t)(j0 + i) * n + j0 + k] * xv[k];
+                    xv[i] = s / rm[(size_t)(j0 + i) * n + j0 + i];
+                }
+                for (int i = 0; i < bs; ++i) inv[i][col] = xv[i];
+            }
+            for (int i = 0; i < 32; ++i)
+                for (int j = 0; j < 32; ++j) {
+                    df[(size_t)b * 1024 + 32 * i + j] = inv[i][j];
+                    db[(size_t)b * 1024 + 32 * i + j] = inv[j][i];  // (L_b^{-1})' = (L_b')^{-1}
+                }
+        }
+        c->n_c = n;
+        c->Lrm = dalloc<double>(c, rm.size());
+        c->Lcm = dalloc<double>(c, cm.size());
+        c->Dinv_f = dalloc<double>(c, df.size());
+        c->Dinv_b = dalloc<double>(c, db.size());
+        CK(cudaMemcpy(c->Lrm, rm.data(), rm.size() * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->Lcm, cm.data(), cm.size() * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->Dinv_f, df.data(), df.size() * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->Dinv_b, db.data(), db.size() * 8, cudaMemcpyHostToDevice));
+        c->coarse_uploaded = true;
+    });
+}
+
+int aspamg_gpu_finalize(aspamg_gpu_ctx* c) {
+    return guard(c, [&] {
+        if (!c) throw Fail{4, "null context"};
+        if (c->finalized) return;
+        CK(cudaSetDevice(c->device));
+        do_finalize(c);
+    });
+}
+
+int aspamg_gpu_num_levels(aspamg_gpu_ctx* c, int64_t* n) {
+    return guard(c, [&] { *n = c ? (int64_t)c->lv.size() : 0; });
+}
+
+int aspamg_gpu_level_info(aspamg_gpu_ctx* c, int64_t level, aspamg_gpu_level_stats* o) {
+    return guard(c, [&] {
+        if (!c || level < 0 || level >= (int64_t)c->lv.size()) throw Fail{1, "level_info: level out of range"};
+        const GLevel& l = c->lv[(size_t)level];
+        std::memset(o, 0, sizeof(*o));
+        o->n = l.n;
+        o->a_format = l.A.fmt;
+        o->a_nnz = l.a_nnz;
+        o->a_nnzb = l.A.fmt == 1 ? l.A.bsr.nnzb : 0;
+        o->a_fill = l.A.fmt == 1 ? 9.0 * l.A.bsr.nnzb / std::max<double>(1.0, (double)l.a_nnz) : 1.0;
+        o->g_nnz = l.has_smoother ? l.G.csr.nnz : 0;
+        o->p_nnz = l.has_smoother ? l.P.csr.nnz : 0;
+        o->omega = l.omega;
+        o->alg_bytes_A = alg_bytes(l.A);
+        if (l.has_smoother) {
+            o->alg_bytes_G = alg_bytes(l.G);
+            o->alg_bytes_Gt = alg_bytes(l.Gt);
+            o->alg_bytes_P = alg_bytes(l.P);
+            o->alg_bytes_Pt = alg_bytes(l.Pt);
+        }
+        o->device_bytes = (double)c->device_bytes;
+    });
+}
+
+int aspamg_gpu_vcycle_device(aspamg_gpu_ctx* c, const double* y, double* z) {
+    return guard(c, [&] {
+        ensure_ready(c);
+        CK(cudaSetDevice(c->device));
+        const size_t bytes = (size_t)c->lv[0].n * sizeof(double);
+        CK(cudaMemcpyAsync(c->vy, y, bytes, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaGraphLaunch(c->vc_exec, c->stream));
+        CK(cudaMemcpyAsync(z, c->vz, bytes, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaGetLastError());
+    });
+}
+
+int aspamg_gpu_vcycle(aspamg_gpu_ctx* c, const double* y, double* z) {
+    return guard(c, [&] {
+        ensure_ready(c);
+        if (!y || !z) throw Fail{1, "vcycle: null buffer"};
+        CK(cudaSetDevice(c->device));
+        const size_t bytes = (size_t)c->lv[0].n * sizeof(double);
+        CK(cudaMemcpyAsync(c->vy, y, bytes, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaGraphLaunch(c->vc_exec, c->stream));
+        CK(cudaMemcpyAsync(z, c->vz, bytes, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaGetLastError());
+    });
+}
+
+int aspamg_gpu_spmv(aspamg_gpu_ctx* c, int64_t level, int which, const double* x, double* y) {
+    return guard(c, [&] {
+        ensure_ready(c);
+        if (level < 0 || level >= (int64_t)c->lv.size()) throw Fail{1, "spmv: level out of range"};
+        const GLevel& l = c->lv[(size_t)level];
+        if (which != 0 && !l.has_smoother) throw Fail{1, "spmv: operand absent on the coarsest level"};
+        const DMat* M = which == 0 ? &l.A : which == 1 ? &l.G : which == 2 ? &l.Gt : which == 3 ? &l.P : which == 4 ? &l.Pt : nullptr;
+        if (!M) throw Fail{4, "spmv: which must be 0..4"};
+        CK(cudaSetDevice(c->device));
+        double *dx = nullptr, *dy = nullptr;
+        CK(cudaMalloc(&dx, sizeof(double) * std::max(1, M->cols())));
+        CK(cudaMalloc(&dy, sizeof(double) * std::max(1, M->rows())));
+        cudaMemcpyAsync(dx, x, sizeof(double) * M->cols(), cudaMemcpyHostToDevice, c->stream);
+        spmv(*M, EPI_PLAIN, dx, dy, nullptr, 1.0, nullptr, Red{}, nullptr, Launch{0, c->stream});
+        cudaMemcpyAsync(y, dy, sizeof(double) * M->rows(), cudaMemcpyDeviceToHost, c->stream);
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        cudaFree(dx);
+        cudaFree(dy);
+        CK(e);
+        CK(cudaGetLastError());
+    });
+}
+
+int aspamg_gpu_smooth(aspamg_gpu_ctx* c, int64_t level, const double* b, const double* x, double* out) {
+    return guard(c, [&] {
+        ensure_ready(c);
+        if (level < 0 || level + 1 >= (int64_t)c->lv.size()) throw Fail{1, "smooth: level has no smoother"};
+        GLevel& l = c->lv[(size_t)level];
+        CK(cudaSetDevice(c->device));
+        const size_t bytes = sizeof(double) * l.n;
+        double *db = nullptr, *dx = nullptr;
+        CK(cudaMalloc(&db, bytes));
+        CK(cudaMalloc(&dx, bytes));
+        cudaStream_t s = c->stream;
+        cudaMemcpyAsync(db, b, bytes, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dx, x, bytes, cudaMemcpyHostToDevice, s);
+        // r = b - A x ; t = G r ; x' = x + w G' t (in place)
+        spmv(l.A, EPI_RESID, dx, l.r, db, 1.0, nullptr, Red{}, nullptr, Launch{0, s});
+        spmv(l.G, EPI_PLAIN, l.r, l.t, nullptr, 1.0, nullptr, Red{}, nullptr, Launch{0, s});
+        spmv(l.Gt, EPI_ADDSCALE, l.t, dx, dx, l.omega, nullptr, Red{}, nullptr, Launch{0, s});
+        cudaMemcpyAsync(out, dx, bytes, cudaMemcpyDeviceToHost, s);
+        cudaError_t e = cudaStreamSynchronize(s);
+        cudaFree(db);
+        cudaFree(dx);
+        CK(e);
+        CK(cudaGetLastError());
+    });
+}
+
+int aspamg_gpu_coarse_solve(aspamg_gpu_ctx* c, const double* y, double* z) {
+    return guard(c, [&] {
+        ensure_ready(c);
+        CK(cudaSetDevice(c->device));
+        const size_t bytes = sizeof(double) * c->n_c;
+        double *dy = nullptr, *dz = nullptr;
+        CK(cudaMalloc(&dy, bytes));
+        CK(cudaMalloc(&dz, bytes));
+        cudaMemcpyAsync(dy, y, bytes, cudaMemcpyHostToDevice, c->stream);
+        coarse_solve(c->n_c, c->Lrm, c->Lcm, c->Dinv_f, c->Dinv_b, dy, dz, nullptr, Red{}, nullptr, Launch{1, c->stream});
+        cudaMemcpyAsync(z, dz, bytes, cudaMemcpyDeviceToHost, c->stream);
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        cudaFree(dy);
+        cudaFree(dz);
+        CK(e);
+        CK(cudaGetLastError());
+    });
+}
+
+int aspamg_gpu_pcg(aspamg_gpu_ctx* c, const double* b, const double* x0, double rel_tol, int64_t max_it, double* x,
+                   double* history, int64_t* n_it, int* converged, double* true_rel_res) {
+    int status = 0;
+    int code = guard(c, [&] {
+        ensure_ready(c);
+        if (!b || !x || !n_it || !converged || !true_rel_res) throw Fail{1, "pcg: null argument"};
+        CK(cudaSetDevice(c->device));
+        const size_t bytes = sizeof(double) * c->lv[0].n;
+        CK(cudaMemcpyAsync(c->b, b, bytes, cudaMemcpyHostToDevice, c->stream));
+        if (x0) CK(cudaMemcpyAsync(c->x, x0, bytes, cudaMemcpyHostToDevice, c->stream));
+        long long it = 0;
+        int conv = 0;
+        double trr = 0;
+        try {
+            status = run_pcg(c, x0 != nullptr, rel_tol, max_it, &it, &conv, &trr);
+        } catch (const Fail& f) {
+            *n_it = it;
+            throw;
+        }
+        CK(cudaMemcpyAsync(x, c->x, bytes, cudaMemcpyDeviceToHost, c->stream));
+        if (history && it > 0) CK(cudaMemcpyAsync(history, c->hist, sizeof(double) * it, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaGetLastError());
+        *n_it = it;
+        *converged = conv;
+        *true_rel_res = trr;
+    });
+    if (code != 0) return code;
+    if (status == 6) c->err = "pcg: not converged";
+    return status;
+}
+
+int aspamg_gpu_pcg_device(aspamg_gpu_ctx* c, const double* b, const double* x0, double rel_tol, int64_t max_it,
+                          double* x, double* history, int64_t* n_it, int* converged, double* true_rel_res) {
+    int status = 0;
+    int code = guard(c, [&] {
+        ensure_ready(c);
+        if (!b || !x || !n_it || !converged || !true_rel_res) throw Fail{1, "pcg: null argument"};
+        CK(cudaSetDevice(c->device));
+        const size_t bytes = sizeof(double) * c->lv[0].n;
+        CK(cudaMemcpyAsync(c->b, b, bytes, cudaMemcpyDeviceToDevice, c->stream));
+        if (x0) CK(cudaMemcpyAsync(c->x, x0, bytes, cudaMemcpyDeviceToDevice, c->stream));
+        long long it = 0;
+        int conv = 0;
+        double trr = 0;
+        status = run_pcg(c, x0 != nullptr, rel_tol, max_it, &it, &conv, &trr);
+        CK(cudaMemcpyAsync(x, c->x, bytes, cudaMemcpyDeviceToDevice, c->stream));
+        if (history && it > 0) CK(cudaMemcpyAsync(history, c->hist, sizeof(double) * it, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaGetLastError());
+        *n_it = it;
+        *converged = conv;
+        *true_rel_res = trr;
+    });
+    if (code != 0) return code;
+    if (status == 6) c->err = "pcg: not converged";
+    return status;
+}
+
+int aspamg_gpu_last_solve_ms(aspamg_gpu_ctx* c, double* ms) {
+    return guard(c, [&] { *ms = c ? c->last_ms : 0.0; });
+}
+
+int aspamg_gpu_launch_count(aspamg_gpu_ctx* c, int64_t* n) {
+    return guard(c, [&] { *n = c ? c->last_launches : 0; });
+}
+
+// One PCG iteration's ops run eagerly with an event pair around each kernel.
+int aspamg_gpu_profile_iteration(aspamg_gpu_ctx* c, aspamg_gpu_kernel_time* out, int cap, int* count) {
+    return guard(c, [&] {
+        ensure_ready(c);
+        CK(cudaSetDevice(c->device));
+        cudaStream_t s = c->stream;
+        // a live, non-terminating state: k = 1 (beta path), tol 0, huge max_it
+        PcgState h = {};
+        CK(cudaMemcpyAsync(c->st_host, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        h = *c->st_host;
+        h.done = 0; h.notspd = 0; h.k = 1; h.tol = 0.0; h.max_it = 1ll << 40; h.history = c->hist;
+        if (!(h.bnorm > 0)) h.bnorm = 1.0;
+        if (!(h.rz != 0)) h.rz = 1.0;
+        if (!c->hist) {
+            c->hist_cap = 1024;
+            CK(cudaMalloc(&c->hist, (size_t)c->hist_cap * sizeof(double)));
+            h.history = c->hist;
+        }
+        *c->st_host = h;
+        CK(cudaMemcpyAsync(c->st, c->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+        std::vector<cudaEvent_t> ev(c->body.size() + 1);
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        // warm the iteration once
+        run_ops(c->body, s);
+        CK(cudaMemcpyAsync(c->st, c->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(ev[0], s));
+        for (size_t i = 0; i < c->body.size(); ++i) {
+            c->body[i].fn(s);
+            CK(cudaEventRecord(ev[i + 1], s));
+        }
+        CK(cudaStreamSynchronize(s));
+        int k = 0;
+        for (size_t i = 0; i < c->body.size() && k < cap; ++i, ++k) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+            std::memset(&out[k], 0, sizeof(out[k]));
+            std::strncpy(out[k].name, c->body[i].name.c_str(), sizeof(out[k].name) - 1);
+            out[k].level = c->body[i].level;
+            out[k].ms = ms;
+            out[k].alg_bytes = c->body[i].bytes;
+        }
+        *count = k;
+        for (auto& e : ev) cudaEventDestroy(e);
+        CK(cudaGetLastError());
+    });
+}
+
+int aspamg_gpu_time_kernel(aspamg_gpu_ctx* c, const char* name, int64_t level, int reps, double* avg_ms,
+                           double* bytes) {
+    return guard(c, [&] {
+        ensure_ready(c);
+        CK(cudaSetDevice(c->device));
+        const Op* op = nullptr;
+        for (const auto& o : c->body)
+            if (o.level == level && (o.name == name || o.name.rfind(std::string(name) + ".", 0) == 0)) { op = &o; break; }
+        if (!op) throw Fail{4, std::string("time_kernel: no op named ") + name + " at that level"};
+        cudaStream_t s = c->stream;
+        PcgState h = {};
+        CK(cudaMemcpyAsync(c->st_host, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        h = *c->st_host;
+        h.done = 0; h.notspd = 0; h.k = 1; h.tol = 0.0; h.max_it = 1ll << 40;
+        if (!c->hist) {
+            c->hist_cap = 1024;
+            CK(cudaMalloc(&c->hist, (size_t)c->hist_cap * sizeof(double)));
+        }
+        h.history = c->hist;
+        if (!(h.bnorm > 0)) h.bnorm = 1.0;
+        if (!(h.rz != 0)) h.rz = 1.0;
+        *c->st_host = h;
+        CK(cudaMemcpyAsync(c->st, c->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+        for (int i = 0; i < 3; ++i) op->fn(s);
+        CK(cudaEventRecord(c->ev0, s));
+        for (int i = 0; i < reps; ++i) op->fn(s);
+        CK(cudaEventRecord(c->ev1, s));
+        CK(cudaStreamSynchronize(s));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        *avg_ms = ms / std::max(1, reps);
+        *bytes = op->bytes;
+        CK(cudaGetLastError());
+    });
+}
+
+int aspamg_gpu_stream(aspamg_gpu_ctx* c, void** s) {
+    return guard(c, [&] { *s = c ? (void*)c->stream : nullptr; });
+}
+
+int aspamg_gpu_alloc_pinned(int64_t bytes, void** out) {
+    return guard(nullptr, [&] { CK(cudaMallocHost(out, (size_t)std::max<int64_t>(bytes, 1))); });
+}
+
+int aspamg_gpu_free_pinned(void* p) {
+    return guard(nullptr, [&] { CK(cudaFreeHost(p)); });
+}
+
+int aspamg_gpu_alloc_device(aspamg_gpu_ctx* c, int64_t bytes, void** out) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaMalloc(out, (size_t)std::max<int64_t>(bytes, 1)));
+    });
+}
+
+int aspamg_gpu_free_device(aspamg_gpu_ctx* c, void* p) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaFree(p));
+    });
+}
+
+int aspamg_gpu_memcpy(aspamg_gpu_ctx* c, void* dst, const void* src, int64_t bytes) {
+    return guard(c, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+}  // extern "C"

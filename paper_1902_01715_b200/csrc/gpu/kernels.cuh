@@ -1,0 +1,116 @@
+// Device data layout + kernel launchers for the sm_100a solve path.
+//
+// Everything is fp64 on CUDA cores: the path is sparse and HBM-bound
+// ("None use tensor cores"). Indices are int32 on the device
+// (all configs have nnz < 2^31), which cuts index traffic vs the reference's
+// int64 CSR (sparse_matrix.hpp:27-33).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace aspamg_gpu {
+
+constexpr int kBlock = 256;  // threads per CTA for every streaming kernel
+
+// CSR, int32 offsets/columns. `group` = threads cooperating on one row
+// (power of two, 1..32), chosen from the mean row length at finalize.
+struct DCsr {
+    int n_rows = 0, n_cols = 0;
+    long long nnz = 0;
+    int* rp = nullptr;
+    int* ci = nullptr;
+    double* v = nullptr;
+    int group = 1;
+    bool stream = false;  // evict-first loads (matrix larger than ~L2/2)
+};
+
+// Exact 3x3 block CSR: nb block rows, values block-major (9 per block,
+// row-major inside the block), one int32 block column per block.
+struct DBsr3 {
+    int nb = 0, nbc = 0;
+    long long nnzb = 0;
+    int* rp = nullptr;
+    int* ci = nullptr;
+    double* v = nullptr;
+    bool stream = false;
+};
+
+// One matrix operand: BSR3 when the CSR is exactly 3x3-blocked, else CSR.
+struct DMat {
+    int fmt = 0;  // 0 CSR, 1 BSR3
+    DCsr csr;
+    DBsr3 bsr;
+    int rows() const { return fmt == 1 ? 3 * bsr.nb : csr.n_rows; }
+    int cols() const { return fmt == 1 ? 3 * bsr.nbc : csr.n_cols; }
+};
+
+// Epilogue of y = f(M x):
+enum Epi : int {
+    EPI_PLAIN = 0,     // y = Mx
+    EPI_SCALE = 1,     // y = omega * Mx
+    EPI_RESID = 2,     // y = aux - Mx
+    EPI_ADD = 3,       // y = aux + Mx
+    EPI_ADDSCALE = 4,  // y = aux + omega * Mx
+};
+
+// What the last CTA does with a finished deterministic reduction.
+enum Fin : int {
+    FIN_NONE = 0,
+    FIN_STORE = 1,   // out[0] = sum
+    FIN_PQ = 2,      // PCG: pq = sum; alpha = rz/pq; pq <= 0 -> not SPD, done
+    FIN_RZ = 3,      // PCG: beta = (k == 0) ? 0 : sum/rz ; rz = sum
+    FIN_RR = 4,      // PCG: history[k] = sqrt(sum)/||b||; k++; convergence test
+    FIN_INIT = 5,    // PCG init (two sums: b.b, r.r)
+};
+
+// Device-resident PCG state (one per context). Host reads it once per solve.
+struct PcgState {
+    double rz, pq, alpha, beta, bnorm, tol, rr, trr2;
+    long long k, max_it;
+    int done, notspd, converged, pad;
+    double* history;
+};
+
+// Deterministic two-pass reduction site: every CTA writes its fixed-order
+// partial, the last CTA to arrive (atomic ticket) sums the partials in index
+// order -> same bits for every run, no floating-point atomics.
+struct Red {
+    double* partials = nullptr;   // >= gridDim.x (x2 for FIN_INIT)
+    unsigned* counter = nullptr;
+    int fin = FIN_NONE;
+    double* out = nullptr;
+    PcgState* st = nullptr;
+    unsigned long long cond = 0;  // cudaGraphConditionalHandle for FIN_RR (0 = none)
+    int use_cond = 0;
+};
+
+struct Launch {
+    int grid = 0;
+    cudaStream_t stream = nullptr;
+};
+
+// y = epi(M x); optional dot sum_i y_i * dotw_i reduced through `red`.
+// `done` (device int) makes the kernel a no-op once the solve has finished.
+void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux, double omega,
+          const double* dotw, const Red& red, const int* done, const Launch& L);
+int spmv_grid(const DMat& M);
+
+// p = (k == 0) ? z : z + beta p
+void pcg_p(int n, const double* z, double* p, const PcgState* st, const int* done, const Launch& L);
+// x += alpha p ; r -= alpha q ; rr = r.r -> FIN_RR
+void pcg_xr(int n, double* x, double* r, const double* p, const double* q, const Red& red, const int* done,
+            const Launch& L);
+// b.b and r.r -> FIN_INIT
+void pcg_init_dots(int n, const double* b, const double* r, const Red& red, const Launch& L);
+int vec_grid(int n);
+
+// Coarsest level: L L' z = y by blocked substitution (one CTA). Lrm: row-major
+// lower factor; Lcm: column-major (= row-major L'); Dinv: inverted 32x32
+// diagonal blocks (row-major, per block). Optional dot z.dotw -> red.
+void coarse_solve(int n, const double* Lrm, const double* Lcm, const double* Dinv_f, const double* Dinv_b,
+                  const double* y, double* z, const double* dotw, const Red& red, const int* done, const Launch& L);
+
+void fill_zero(int n, double* y, const int* done, const Launch& L);
+
+}  // namespace aspamg_gpu

@@ -1,0 +1,201 @@
+// C-ABI over the host setup (include/aspamg_host.h).
+#include "../../../include/aspamg_host.h"
+
+#include "amg.hpp"
+#include "fem.hpp"
+
+#include <new>
+#include <string>
+
+using namespace aspamg;
+
+struct aspamg_problem {
+    GeneratedProblem p;
+    std::vector<double> rhs;
+};
+struct aspamg_hierarchy {
+    Hierarchy h;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const DimensionError& e) { g_err = e.what(); return 1; }
+    catch (const NotSpdError& e) { g_err = e.what(); return 2; }
+    catch (const NumericalError& e) { g_err = e.what(); return 3; }
+    catch (const ConfigError& e) { g_err = e.what(); return 4; }
+    catch (const IoError& e) { g_err = e.what(); return 7; }
+    catch (const std::bad_alloc&) { g_err = "out of host memory"; return 5; }
+    catch (const std::exception& e) { g_err = e.what(); return 5; }
+    catch (...) { g_err = "unknown error"; return 5; }
+}
+
+aspamg_csr_view view(const Csr& m) {
+    aspamg_csr_view v{};
+    v.n_rows = m.n_rows;
+    v.n_cols = m.n_cols;
+    v.nnz = m.nnz();
+    v.row_offsets = m.rowptr.empty() ? nullptr : m.rowptr.data();
+    v.col_indices = m.col.data();
+    v.values = m.val.data();
+    return v;
+}
+
+Csr from_view(const aspamg_csr_view& v) {
+    if (v.n_rows < 0 || v.n_cols < 0) throw DimensionError("csr view: negative size");
+    if (!v.row_offsets) throw DimensionError("csr view: null row_offsets");
+    Csr m;
+    m.n_rows = v.n_rows;
+    m.n_cols = v.n_cols;
+    m.rowptr.assign(v.row_offsets, v.row_offsets + v.n_rows + 1);
+    const index_t nnz = m.rowptr.back();
+    if (m.rowptr[0] != 0 || nnz < 0) throw DimensionError("csr view: bad row_offsets");
+    for (index_t i = 0; i < m.n_rows; ++i)
+        if (m.rowptr[static_cast<size_t>(i) + 1] < m.rowptr[static_cast<size_t>(i)])
+            throw DimensionError("csr view: row_offsets not non-decreasing");
+    m.col.assign(v.col_indices, v.col_indices + nnz);
+    m.val.assign(v.values, v.values + nnz);
+    for (index_t i = 0; i < m.n_rows; ++i)
+        for (index_t q = m.rowptr[static_cast<size_t>(i)]; q < m.rowptr[static_cast<size_t>(i) + 1]; ++q) {
+            const index_t c = m.col[static_cast<size_t>(q)];
+            if (c < 0 || c >= m.n_cols) throw DimensionError("csr view: column index out of range");
+            if (q > m.rowptr[static_cast<size_t>(i)] && c <= m.col[static_cast<size_t>(q) - 1])
+                throw DimensionError("csr view: columns must be sorted and unique per row");
+        }
+    return m;
+}
+}  // namespace
+
+extern "C" {
+
+const char* aspamg_host_last_error(void) { return g_err.c_str(); }
+int aspamg_host_set_threads(int n) { set_num_threads(n); return 0; }
+int aspamg_host_get_threads(void) { return num_threads(); }
+
+int aspamg_problem_config(int cfg, int64_t scale, aspamg_problem** out) {
+    return guard([&] {
+        auto* p = new aspamg_problem;
+        try { p->p = make_config(cfg, scale, p->rhs); } catch (...) { delete p; throw; }
+        *out = p;
+    });
+}
+
+int aspamg_problem_hex(int64_t nx, int64_t ny, int64_t nz, double spacing, double young, double poisson,
+                       uint32_t clamp_faces, aspamg_problem** out) {
+    return guard([&] {
+        MeshSpec m;
+        m.nx = nx; m.ny = ny; m.nz = nz;
+        m.hx = m.hy = m.hz = spacing;
+        m.clamped = clamp_faces;
+        if (nx < 1 || ny < 1 || nz < 1) throw ConfigError("assembly: element counts must be >= 1");
+        std::vector<Material> mats(static_cast<size_t>(nx * ny * nz), Material{young, poisson});
+        auto* p = new aspamg_problem;
+        try {
+            p->p = assemble_hex(m, mats);
+            p->rhs = rhs_ones(p->p);
+        } catch (...) { delete p; throw; }
+        *out = p;
+    });
+}
+
+int aspamg_problem_matrix(const aspamg_problem* p, aspamg_csr_view* out) {
+    return guard([&] { *out = view(p->p.stiffness); });
+}
+int aspamg_problem_rhs(const aspamg_problem* p, const double** rhs, int64_t* n) {
+    return guard([&] { *rhs = p->rhs.data(); *n = static_cast<int64_t>(p->rhs.size()); });
+}
+int aspamg_problem_coords(const aspamg_problem* p, const double** xyz, int64_t* n_nodes) {
+    return guard([&] { *xyz = p->p.coords.data(); *n_nodes = p->p.n_free; });
+}
+void aspamg_problem_free(aspamg_problem* p) { delete p; }
+
+int aspamg_setup_config_default(aspamg_setup_config* c) {
+    return guard([&] {
+        HierarchyConfig h;
+        c->k0 = h.smoother.k0; c->rho0 = h.smoother.rho0; c->eps0 = h.smoother.eps0;
+        c->ki = h.smoother.ki; c->rhoi = h.smoother.rhoi; c->epsi = h.smoother.epsi;
+        c->omega_bar = h.smoother.omega_bar; c->rho_bar = h.smoother.rho_bar;
+        c->lanczos_steps = h.smoother.lanczos_steps;
+        c->n_tv = h.srqcg.n_tv; c->n_rq = h.srqcg.k_max; c->k_ritz = h.srqcg.k_ritz; c->srqcg_tol = h.srqcg.residual_tol;
+        c->theta = h.theta; c->d_p = h.dpls.d_p; c->n_max = h.dpls.n_max; c->eps_p = h.dpls.eps_p; c->kappa_p = h.dpls.kappa_p;
+        c->max_levels = h.max_levels; c->min_coarse_size = h.min_coarse_size; c->nu1 = h.nu1; c->nu2 = h.nu2;
+        c->seed = h.smoother.seed;
+    });
+}
+
+int aspamg_setup(const aspamg_csr_view* A, const double* coords, int64_t n_nodes, const aspamg_setup_config* c,
+                 aspamg_hierarchy** out) {
+    return guard([&] {
+        if (!A || !c || !out) throw ConfigError("aspamg_setup: null argument");
+        HierarchyConfig h;
+        h.smoother.k0 = c->k0; h.smoother.rho0 = c->rho0; h.smoother.eps0 = c->eps0;
+        h.smoother.ki = c->ki; h.smoother.rhoi = c->rhoi; h.smoother.epsi = c->epsi;
+        h.smoother.omega_bar = c->omega_bar; h.smoother.rho_bar = c->rho_bar;
+        h.smoother.lanczos_steps = c->lanczos_steps; h.smoother.seed = c->seed;
+        h.srqcg.n_tv = c->n_tv; h.srqcg.k_max = c->n_rq; h.srqcg.k_ritz = c->k_ritz;
+        h.srqcg.residual_tol = c->srqcg_tol; h.srqcg.seed = c->seed;
+        h.theta = c->theta;
+        h.dpls.d_p = c->d_p; h.dpls.n_max = c->n_max; h.dpls.eps_p = c->eps_p; h.dpls.kappa_p = c->kappa_p;
+        h.max_levels = c->max_levels; h.min_coarse_size = c->min_coarse_size; h.nu1 = c->nu1; h.nu2 = c->nu2;
+        if (h.srqcg.n_tv < 1 || h.srqcg.k_ritz < 1 || h.smoother.lanczos_steps < 1)
+            throw ConfigError("aspamg_setup: n_tv, k_ritz, lanczos_steps must be >= 1");
+        Csr K = from_view(*A);
+        K.symmetric = true;
+        std::vector<double> xyz;
+        if (coords && n_nodes > 0) {
+            if (3 * n_nodes != K.n_rows) throw DimensionError("aspamg_setup: coordinates do not match 3 dofs per node");
+            xyz.assign(coords, coords + 3 * n_nodes);
+        }
+        auto* hh = new aspamg_hierarchy;
+        try { hh->h = amg_setup(K, xyz, h); } catch (...) { delete hh; throw; }
+        *out = hh;
+    });
+}
+
+int aspamg_hierarchy_info_get(const aspamg_hierarchy* hh, aspamg_hierarchy_info* o) {
+    return guard([&] {
+        const Hierarchy& h = hh->h;
+        o->n_levels = static_cast<int64_t>(h.levels.size());
+        o->n_coarse = h.n_coarse; o->nu1 = h.nu1; o->nu2 = h.nu2;
+        o->C_gd = h.C_gd; o->C_op = h.C_op; o->C_fs = h.C_fs;
+        o->T_ts = h.t.T_ts; o->T_cs = h.t.T_cs; o->T_sm = h.t.T_sm; o->T_pl = h.t.T_pl; o->T_rap = h.t.T_rap; o->T_p = h.t.T_p;
+    });
+}
+
+int aspamg_hierarchy_level(const aspamg_hierarchy* hh, int64_t l, aspamg_level_view* o) {
+    return guard([&] {
+        const Hierarchy& h = hh->h;
+        if (l < 0 || l >= static_cast<int64_t>(h.levels.size())) throw DimensionError("hierarchy: level out of range");
+        const Level& L = h.levels[static_cast<size_t>(l)];
+        o->A = view(L.A); o->G = view(L.smoother.G); o->Gt = view(L.Gt); o->P = view(L.P); o->Pt = view(L.Pt);
+        o->omega = L.smoother.omega; o->lambda_hat = L.smoother.lambda_hat; o->kaporin_estimate = L.smoother.kaporin_estimate;
+        o->refinement_passes = L.smoother.refinement_passes;
+        o->smoother_exit = static_cast<int32_t>(L.smoother.exit_reason);
+        o->n_tv = L.n_tv;
+    });
+}
+
+int aspamg_hierarchy_coarse(const aspamg_hierarchy* hh, int64_t* n_c, const double** L) {
+    return guard([&] { *n_c = hh->h.n_coarse; *L = hh->h.coarse_L.data(); });
+}
+
+int aspamg_hierarchy_save(const aspamg_hierarchy* hh, const char* path) {
+    return guard([&] { hierarchy_save(hh->h, path); });
+}
+
+int aspamg_hierarchy_load(const char* path, aspamg_hierarchy** out) {
+    return guard([&] {
+        auto* hh = new aspamg_hierarchy;
+        try { hh->h = hierarchy_load(path); } catch (...) { delete hh; throw; }
+        *out = hh;
+    });
+}
+
+void aspamg_hierarchy_free(aspamg_hierarchy* h) { delete h; }
+
+}  // extern "C"

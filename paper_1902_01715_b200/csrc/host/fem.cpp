@@ -1,0 +1,478 @@
+// Structured hex elasticity generator; see fem.hpp for the reference mapping.
+#include "fem.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <omp.h>
+
+namespace aspamg {
+
+// fem.cpp:9-14
+void Material::validate() const {
+    if (!(young_modulus > 0.0) || !std::isfinite(young_modulus))
+        throw ConfigError("material: Young modulus must be positive");
+    if (!(poisson_ratio > -1.0) || !(poisson_ratio < 0.5))
+        throw ConfigError("material: Poisson ratio must lie in (-1, 0.5)");
+}
+
+namespace {
+
+// fem.cpp:18-28 (isotropic D in Voigt order xx,yy,zz,xy,yz,zx)
+void elastic_matrix(const Material& m, double D[6][6]) {
+    const double E = m.young_modulus, nu = m.poisson_ratio;
+    const double lambda = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    const double mu = E / (2.0 * (1.0 + nu));
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) D[i][j] = 0.0;
+    D[0][0] = D[1][1] = D[2][2] = lambda + 2.0 * mu;
+    D[0][1] = D[0][2] = D[1][0] = D[1][2] = D[2][0] = D[2][1] = lambda;
+    D[3][3] = D[4][4] = D[5][5] = mu;
+}
+
+// fem.cpp:30-34: local node a = ia + 2 ja + 4 ka
+constexpr double kSign[8][3] = {{-1, -1, -1}, {1, -1, -1}, {-1, 1, -1}, {1, 1, -1},
+                                {-1, -1, 1},  {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
+
+// Accumulate det * B' D B for one Gauss point given physical gradients.
+void add_btdb(const double grad[8][3], const double D[6][6], double det, double K[24][24]) {
+    double B[6][24];
+    for (int r = 0; r < 6; ++r)
+        for (int c = 0; c < 24; ++c) B[r][c] = 0.0;
+    for (int a = 0; a < 8; ++a) {  // fem.cpp:67-78
+        const double dx = grad[a][0], dy = grad[a][1], dz = grad[a][2];
+        B[0][3 * a + 0] = dx;
+        B[1][3 * a + 1] = dy;
+        B[2][3 * a + 2] = dz;
+        B[3][3 * a + 0] = dy;
+        B[3][3 * a + 1] = dx;
+        B[4][3 * a + 1] = dz;
+        B[4][3 * a + 2] = dy;
+        B[5][3 * a + 0] = dz;
+        B[5][3 * a + 2] = dx;
+    }
+    double BtD[24][6];
+    for (int i = 0; i < 24; ++i)
+        for (int k = 0; k < 6; ++k) {
+            double s = 0.0;
+            for (int l = 0; l < 6; ++l) s += B[l][i] * D[l][k];
+            BtD[i][k] = s;
+        }
+    for (int i = 0; i < 24; ++i)
+        for (int j = 0; j < 24; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 6; ++k) s += BtD[i][k] * B[k][j];
+            K[i][j] += det * s;
+        }
+}
+
+void mirror_lower(double K[24][24]) {  // fem.cpp:81-83
+    for (int i = 0; i < 24; ++i)
+        for (int j = 0; j < i; ++j) K[j][i] = K[i][j];
+}
+
+}  // namespace
+
+// fem.cpp:37-85 (regular grid: constant Jacobian 2/h, det h^3/8)
+void hex_element_stiffness_cube(double h, const Material& m, double Ke[24][24]) {
+    m.validate();
+    if (!(h > 0.0)) throw ConfigError("assembly: spacing must be positive");
+    double D[6][6];
+    elastic_matrix(m, D);
+    const double gp = 1.0 / std::sqrt(3.0);
+    const double det_j = h * h * h / 8.0;
+    for (int i = 0; i < 24; ++i)
+        for (int j = 0; j < 24; ++j) Ke[i][j] = 0.0;
+    double grad[8][3];
+    for (int gx = 0; gx < 2; ++gx)
+        for (int gy = 0; gy < 2; ++gy)
+            for (int gz = 0; gz < 2; ++gz) {
+                const double xi = gp * (2 * gx - 1), eta = gp * (2 * gy - 1), zeta = gp * (2 * gz - 1);
+                const double scale = 2.0 / h;
+                for (int a = 0; a < 8; ++a) {
+                    const double sx = kSign[a][0], sy = kSign[a][1], sz = kSign[a][2];
+                    grad[a][0] = 0.125 * sx * (1.0 + sy * eta) * (1.0 + sz * zeta) * scale;
+                    grad[a][1] = 0.125 * sy * (1.0 + sx * xi) * (1.0 + sz * zeta) * scale;
+                    grad[a][2] = 0.125 * sz * (1.0 + sx * xi) * (1.0 + sy * eta) * scale;
+                }
+                add_btdb(grad, D, det_j, Ke);
+            }
+    mirror_lower(Ke);
+}
+
+// General isoparametric trilinear hex (extension for distorted meshes, C3).
+void hex_element_stiffness(const double xyz[8][3], const Material& m, double Ke[24][24]) {
+    m.validate();
+    double D[6][6];
+    elastic_matrix(m, D);
+    const double gp = 1.0 / std::sqrt(3.0);
+    for (int i = 0; i < 24; ++i)
+        for (int j = 0; j < 24; ++j) Ke[i][j] = 0.0;
+    for (int gx = 0; gx < 2; ++gx)
+        for (int gy = 0; gy < 2; ++gy)
+            for (int gz = 0; gz < 2; ++gz) {
+                const double xi = gp * (2 * gx - 1), eta = gp * (2 * gy - 1), zeta = gp * (2 * gz - 1);
+                double dn[8][3];
+                for (int a = 0; a < 8; ++a) {
+                    const double sx = kSign[a][0], sy = kSign[a][1], sz = kSign[a][2];
+                    dn[a][0] = 0.125 * sx * (1.0 + sy * eta) * (1.0 + sz * zeta);
+                    dn[a][1] = 0.125 * sy * (1.0 + sx * xi) * (1.0 + sz * zeta);
+                    dn[a][2] = 0.125 * sz * (1.0 + sx * xi) * (1.0 + sy * eta);
+                }
+                double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // J[i][j] = dx_j/dxi_i
+                for (int a = 0; a < 8; ++a)
+                    for (int i = 0; i < 3; ++i)
+                        for (int j = 0; j < 3; ++j) J[i][j] += dn[a][i] * xyz[a][j];
+                const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+                                   J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                                   J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+                if (!(det > 0.0)) throw NumericalError("assembly: inverted or degenerate element");
+                double Ji[3][3];
+                Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / det;
+                Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+                Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+                Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / det;
+                Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+                Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+                Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / det;
+                Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+                Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+                // grad_x N = J^{-1} grad_xi N
+                double grad[8][3];
+                for (int a = 0; a < 8; ++a)
+                    for (int i = 0; i < 3; ++i)
+                        grad[a][i] = Ji[i][0] * dn[a][0] + Ji[i][1] * dn[a][1] + Ji[i][2] * dn[a][2];
+                add_btdb(grad, D, det, Ke);
+            }
+    mirror_lower(Ke);
+}
+
+GeneratedProblem assemble_hex(const MeshSpec& mesh, const std::vector<Material>& materials) {
+    const index_t nx = mesh.nx, ny = mesh.ny, nz = mesh.nz;
+    if (nx < 1 || ny < 1 || nz < 1) throw ConfigError("assembly: element counts must be >= 1");
+    if (!(mesh.hx > 0.0) || !(mesh.hy > 0.0) || !(mesh.hz > 0.0))
+        throw ConfigError("assembly: spacing must be positive");
+    const index_t n_el = nx * ny * nz;
+    if (static_cast<index_t>(materials.size()) != n_el)
+        throw ConfigError("assembly: one material per element required");
+    for (const auto& m : materials) m.validate();
+
+    const index_t mx = nx + 1, my = ny + 1, mz = nz + 1;
+    const index_t n_nodes = mx * my * mz;
+    auto node_id = [&](index_t i, index_t j, index_t k) { return i + mx * (j + my * k); };
+
+    GeneratedProblem P;
+    P.mesh = mesh;
+    P.n_nodes = n_nodes;
+    // Node coordinates (+ interior perturbation, node order, 3 draws per interior node).
+    P.node_xyz.resize(static_cast<size_t>(3 * n_nodes));
+    {
+        Rng rng(mesh.perturb_seed);
+        for (index_t k = 0; k < mz; ++k)
+            for (index_t j = 0; j < my; ++j)
+                for (index_t i = 0; i < mx; ++i) {
+                    const index_t v = node_id(i, j, k);
+                    double x = mesh.hx * double(i), y = mesh.hy * double(j), z = mesh.hz * double(k);
+                    if (mesh.perturb > 0.0 && i > 0 && i < nx && j > 0 && j < ny && k > 0 && k < nz) {
+                        x += rng.symmetric() * mesh.perturb * mesh.hx;
+                        y += rng.symmetric() * mesh.perturb * mesh.hy;
+                        z += rng.symmetric() * mesh.perturb * mesh.hz;
+                    }
+                    P.node_xyz[static_cast<size_t>(3 * v + 0)] = x;
+                    P.node_xyz[static_cast<size_t>(3 * v + 1)] = y;
+                    P.node_xyz[static_cast<size_t>(3 * v + 2)] = z;
+                }
+    }
+    // Clamp (fem.cpp:101-117, extended to a face set) and free numbering (fem.cpp:119-122).
+    auto clamped = [&](index_t i, index_t j, index_t k) {
+        const unsigned c = mesh.clamped;
+        return ((c & FACE_XMIN) && i == 0) || ((c & FACE_XMAX) && i == nx) ||
+               ((c & FACE_YMIN) && j == 0) || ((c & FACE_YMAX) && j == ny) ||
+               ((c & FACE_ZMIN) && k == 0) || ((c & FACE_ZMAX) && k == nz);
+    };
+    P.free_index.assign(static_cast<size_t>(n_nodes), -1);
+    index_t n_free = 0;
+    for (index_t k = 0; k < mz; ++k)
+        for (index_t j = 0; j < my; ++j)
+            for (index_t i = 0; i < mx; ++i)
+                if (!clamped(i, j, k)) P.free_index[static_cast<size_t>(node_id(i, j, k))] = n_free++;
+    P.n_free = n_free;
+    P.coords.resize(static_cast<size_t>(3 * n_free));
+    std::vector<index_t> free_node(static_cast<size_t>(n_free));
+    for (index_t v = 0; v < n_nodes; ++v) {
+        const index_t f = P.free_index[static_cast<size_t>(v)];
+        if (f < 0) continue;
+        free_node[static_cast<size_t>(f)] = v;
+        for (int c = 0; c < 3; ++c)
+            P.coords[static_cast<size_t>(3 * f + c)] = P.node_xyz[static_cast<size_t>(3 * v + c)];
+    }
+
+    // Element stiffness: one per distinct material on undistorted isotropic
+    // cubes (the reference caches by material, fem.cpp:153-158); per element
+    // on distorted / anisotropic meshes.
+    const bool cube = mesh.perturb == 0.0 && mesh.hx == mesh.hy && mesh.hy == mesh.hz;
+    std::vector<int> el_ke(static_cast<size_t>(n_el));
+    std::vector<std::array<double, 576>> ke_table;
+    if (cube) {
+        std::map<std::pair<double, double>, int> seen;
+        for (index_t e = 0; e < n_el; ++e) {
+            const auto key = std::make_pair(materials[static_cast<size_t>(e)].young_modulus,
+                                            materials[static_cast<size_t>(e)].poisson_ratio);
+            auto it = seen.find(key);
+            if (it == seen.end()) {
+                it = seen.emplace(key, static_cast<int>(ke_table.size())).first;
+                ke_table.emplace_back();
+                hex_element_stiffness_cube(mesh.hx, materials[static_cast<size_t>(e)],
+                                           reinterpret_cast<double(*)[24]>(ke_table.back().data()));
+            }
+            el_ke[static_cast<size_t>(e)] = it->second;
+        }
+    } else {
+        ke_table.resize(static_cast<size_t>(n_el));
+#pragma omp parallel for schedule(static) num_threads(num_threads())
+        for (index_t e = 0; e < n_el; ++e) {
+            const index_t ex = e % nx, ey = (e / nx) % ny, ez = e / (nx * ny);
+            double xyz[8][3];
+            for (int a = 0; a < 8; ++a) {
+                const index_t v = node_id(ex + (a & 1), ey + ((a >> 1) & 1), ez + ((a >> 2) & 1));
+                for (int c = 0; c < 3; ++c) xyz[a][c] = P.node_xyz[static_cast<size_t>(3 * v + c)];
+            }
+            hex_element_stiffness(xyz, materials[static_cast<size_t>(e)],
+                                  reinterpret_cast<double(*)[24]>(ke_table[static_cast<size_t>(e)].data()));
+            el_ke[static_cast<size_t>(e)] = static_cast<int>(e);
+        }
+    }
+
+    // CSR pattern: row node f couples with every free node in its 3x3x3
+    // neighbourhood; neighbours ascend in node id == ascending free id.
+    Csr& K = P.stiffness;
+    K.n_rows = K.n_cols = 3 * n_free;
+    K.symmetric = true;
+    std::vector<index_t> deg(static_cast<size_t>(n_free));
+#pragma omp parallel for schedule(static) num_threads(num_threads())
+    for (index_t f = 0; f < n_free; ++f) {
+        const index_t v = free_node[static_cast<size_t>(f)];
+        const index_t i = v % mx, j = (v / mx) % my, k = v / (mx * my);
+        index_t d = 0;
+        for (index_t dk = -1; dk <= 1; ++dk)
+            for (index_t dj = -1; dj <= 1; ++dj)
+                for (index_t di = -1; di <= 1; ++di) {
+                    const index_t a = i + di, b = j + dj, c = k + dk;
+                    if (a < 0 || a > nx || b < 0 || b > ny || c < 0 || c > nz) continue;
+                    if (P.free_index[static_cast<size_t>(node_id(a, b, c))] >= 0) ++d;
+                }
+        deg[static_cast<size_t>(f)] = d;
+    }
+    K.rowptr.assign(static_cast<size_t>(3 * n_free) + 1, 0);
+    for (index_t f = 0; f < n_free; ++f)
+        for (int c = 0; c < 3; ++c)
+            K.rowptr[static_cast<size_t>(3 * f + c) + 1] = 3 * deg[static_cast<size_t>(f)];
+    for (size_t r = 1; r < K.rowptr.size(); ++r) K.rowptr[r] += K.rowptr[r - 1];
+    K.col.resize(static_cast<size_t>(K.rowptr.back()));
+    K.val.assign(static_cast<size_t>(K.rowptr.back()), -0.0);  // (-0.0) + x == x bit-exactly
+
+#pragma omp parallel for schedule(static) num_threads(num_threads())
+    for (index_t f = 0; f < n_free; ++f) {
+        const index_t v = free_node[static_cast<size_t>(f)];
+        const index_t i = v % mx, j = (v / mx) % my, k = v / (mx * my);
+        int slot[27];  // offset (di,dj,dk) -> neighbour position in the row, or -1
+        int pos = 0;
+        for (int o = 0; o < 27; ++o) {
+            const index_t a = i + (o % 3) - 1, b = j + ((o / 3) % 3) - 1, c = k + (o / 9) - 1;
+            slot[o] = -1;
+            if (a < 0 || a > nx || b < 0 || b > ny || c < 0 || c > nz) continue;
+            const index_t g = P.free_index[static_cast<size_t>(node_id(a, b, c))];
+            if (g < 0) continue;
+            slot[o] = pos;
+            for (int cc = 0; cc < 3; ++cc) {
+                const index_t base = K.rowptr[static_cast<size_t>(3 * f + cc)];
+                for (int cb = 0; cb < 3; ++cb)
+                    K.col[static_cast<size_t>(base + 3 * pos + cb)] = 3 * g + cb;
+            }
+            ++pos;
+        }
+        // Elements containing node v, in element order (ez, ey, ex ascending).
+        for (index_t ez = k - 1; ez <= k; ++ez) {
+            if (ez < 0 || ez >= nz) continue;
+            for (index_t ey = j - 1; ey <= j; ++ey) {
+                if (ey < 0 || ey >= ny) continue;
+                for (index_t ex = i - 1; ex <= i; ++ex) {
+                    if (ex < 0 || ex >= nx) continue;
+                    const index_t el = ex + nx * (ey + ny * ez);
+                    const double* Ke = ke_table[static_cast<size_t>(el_ke[static_cast<size_t>(el)])].data();
+                    const int a = static_cast<int>((i - ex) + 2 * (j - ey) + 4 * (k - ez));
+                    for (int b = 0; b < 8; ++b) {
+                        const index_t bi = ex + (b & 1), bj = ey + ((b >> 1) & 1), bk = ez + ((b >> 2) & 1);
+                        const int o = static_cast<int>((bi - i + 1) + 3 * (bj - j + 1) + 9 * (bk - k + 1));
+                        const int p = slot[o];
+                        if (p < 0) continue;  // clamped neighbour
+                        for (int ca = 0; ca < 3; ++ca) {
+                            const index_t base = K.rowptr[static_cast<size_t>(3 * f + ca)] + 3 * p;
+                            for (int cb = 0; cb < 3; ++cb)
+                                K.val[static_cast<size_t>(base + cb)] += Ke[(3 * a + ca) * 24 + 3 * b + cb];
+                        }
+                    }
+                }
+            }
+        }
+    }
+    return P;
+}
+
+// fem.cpp:192-221
+Dense rigid_body_modes(const std::vector<double>& coords, index_t n, bool* rank_deficient) {
+    double cx = 0, cy = 0, cz = 0;
+    if (n > 0) {  // Eigen colwise().mean(): plain sum / n
+        for (index_t v = 0; v < n; ++v) {
+            cx += coords[static_cast<size_t>(3 * v)];
+            cy += coords[static_cast<size_t>(3 * v + 1)];
+            cz += coords[static_cast<size_t>(3 * v + 2)];
+        }
+        cx /= double(n); cy /= double(n); cz /= double(n);
+    }
+    Dense M(3 * n, 6);
+    for (index_t v = 0; v < n; ++v) {
+        const double dx = coords[static_cast<size_t>(3 * v)] - cx;
+        const double dy = coords[static_cast<size_t>(3 * v + 1)] - cy;
+        const double dz = coords[static_cast<size_t>(3 * v + 2)] - cz;
+        M(3 * v + 0, 0) = 1.0;
+        M(3 * v + 1, 1) = 1.0;
+        M(3 * v + 2, 2) = 1.0;
+        M(3 * v + 1, 3) = -dz; M(3 * v + 2, 3) = dy;   // rotation-x
+        M(3 * v + 0, 4) = dz;  M(3 * v + 2, 4) = -dx;  // rotation-y
+        M(3 * v + 0, 5) = -dy; M(3 * v + 1, 5) = dx;   // rotation-z
+    }
+    const index_t dropped = orthonormalize_columns(M);
+    if (rank_deficient) *rank_deficient = dropped > 0;
+    return M;
+}
+
+std::vector<double> rhs_ones(const GeneratedProblem& p) {
+    return std::vector<double>(static_cast<size_t>(3 * p.n_free), 1.0);
+}
+
+std::vector<double> rhs_top_nodal(const GeneratedProblem& p, double fz) {
+    std::vector<double> b(static_cast<size_t>(3 * p.n_free), 0.0);
+    const auto& m = p.mesh;
+    const index_t mx = m.nx + 1, my = m.ny + 1;
+    for (index_t j = 0; j < my; ++j)
+        for (index_t i = 0; i < mx; ++i) {
+            const index_t f = p.free_index[static_cast<size_t>(i + mx * (j + my * m.nz))];
+            if (f >= 0) b[static_cast<size_t>(3 * f + 2)] = fz;
+        }
+    return b;
+}
+
+std::vector<double> rhs_top_pressure(const GeneratedProblem& p, double pressure) {
+    std::vector<double> b(static_cast<size_t>(3 * p.n_free), 0.0);
+    const auto& m = p.mesh;
+    const index_t mx = m.nx + 1, my = m.ny + 1;
+    const double share = pressure * m.hx * m.hy / 4.0;
+    for (index_t ey = 0; ey < m.ny; ++ey)
+        for (index_t ex = 0; ex < m.nx; ++ex)
+            for (int c = 0; c < 4; ++c) {
+                const index_t i = ex + (c & 1), j = ey + (c >> 1);
+                const index_t f = p.free_index[static_cast<size_t>(i + mx * (j + my * m.nz))];
+                if (f >= 0) b[static_cast<size_t>(3 * f + 2)] -= share;
+            }
+    return b;
+}
+
+std::vector<double> rhs_gaussian(const GeneratedProblem& p, std::uint64_t seed) {
+    Rng rng(seed);
+    std::vector<double> b(static_cast<size_t>(3 * p.n_free));
+    for (auto& x : b) x = rng.gaussian();
+    return b;
+}
+
+GeneratedProblem make_config(int cfg, index_t scale, std::vector<double>& rhs) {
+    if (scale < 1) scale = 1;
+    const std::uint64_t base = 1234;  // SPEC.md:219 global seed; salts per SURVEY.md §8d
+    auto sc = [&](index_t n, index_t lo) { return std::max(lo, n / scale); };
+    MeshSpec mesh;
+    std::vector<Material> mats;
+    switch (cfg) {
+        case 1: {
+            mesh.nx = mesh.ny = mesh.nz = sc(20, 2);
+            mesh.hx = mesh.hy = mesh.hz = 1.0 / double(mesh.nx);
+            mesh.clamped = FACE_ZMIN;
+            mats.assign(static_cast<size_t>(mesh.nx * mesh.ny * mesh.nz), Material{1.0, 0.3});
+            break;
+        }
+        case 2: {
+            mesh.nx = mesh.ny = mesh.nz = sc(64, 2);
+            mesh.hx = mesh.hy = mesh.hz = 1.0 / double(mesh.nx);
+            mesh.clamped = FACE_ZMIN;
+            const index_t nb = 8, bs = std::max<index_t>(1, mesh.nx / nb);
+            const index_t nbx = (mesh.nx + bs - 1) / bs;
+            Rng rng(derive_seed(base, 1));
+            std::vector<double> E(static_cast<size_t>(nbx * nbx * nbx));
+            for (auto& e : E) e = std::pow(10.0, 6.0 * rng.uniform());
+            mats.resize(static_cast<size_t>(mesh.nx * mesh.ny * mesh.nz));
+            for (index_t ez = 0; ez < mesh.nz; ++ez)
+                for (index_t ey = 0; ey < mesh.ny; ++ey)
+                    for (index_t ex = 0; ex < mesh.nx; ++ex) {
+                        const index_t b = ex / bs + nbx * (ey / bs + nbx * (ez / bs));
+                        mats[static_cast<size_t>(ex + mesh.nx * (ey + mesh.ny * ez))] =
+                            Material{E[static_cast<size_t>(b)], 0.3};
+                    }
+            break;
+        }
+        case 3: {
+            mesh.nx = mesh.ny = sc(96, 2);
+            mesh.nz = sc(24, 2);
+            mesh.hx = mesh.hy = 1.0;
+            mesh.hz = 0.05;
+            mesh.perturb = 0.3;
+            mesh.perturb_seed = derive_seed(base, 2);
+            mesh.clamped = FACE_ZMIN;
+            mats.assign(static_cast<size_t>(mesh.nx * mesh.ny * mesh.nz), Material{1.0, 0.3});
+            break;
+        }
+        case 4: {
+            mesh.nx = mesh.ny = sc(400, 2);
+            mesh.nz = 4;
+            mesh.hx = mesh.hy = mesh.hz = 1.0;
+            mesh.clamped = FACE_XMIN | FACE_XMAX | FACE_YMIN | FACE_YMAX;
+            mats.assign(static_cast<size_t>(mesh.nx * mesh.ny * mesh.nz), Material{1.0, 0.49});
+            break;
+        }
+        case 5: {
+            mesh.nx = mesh.ny = mesh.nz = sc(128, 2);
+            const double h = 1.0 / double(mesh.nx);
+            mesh.hx = mesh.hy = mesh.hz = h;
+            mesh.clamped = FACE_ZMIN;
+            Rng rng(derive_seed(base, 4));
+            struct Sphere { double x, y, z, r; };
+            std::vector<Sphere> sp(200);
+            for (auto& s : sp) {
+                s.x = rng.uniform(); s.y = rng.uniform(); s.z = rng.uniform();
+                s.r = (2.0 + 4.0 * rng.uniform()) * h;
+            }
+            mats.resize(static_cast<size_t>(mesh.nx * mesh.ny * mesh.nz));
+            for (index_t ez = 0; ez < mesh.nz; ++ez)
+                for (index_t ey = 0; ey < mesh.ny; ++ey)
+                    for (index_t ex = 0; ex < mesh.nx; ++ex) {
+                        const double cx = (double(ex) + 0.5) * h, cy = (double(ey) + 0.5) * h,
+                                     cz = (double(ez) + 0.5) * h;
+                        bool in = false;
+                        for (const auto& s : sp) {
+                            const double dx = cx - s.x, dy = cy - s.y, dz = cz - s.z;
+                            if (dx * dx + dy * dy + dz * dz <= s.r * s.r) { in = true; break; }
+                        }
+                        mats[static_cast<size_t>(ex + mesh.nx * (ey + mesh.ny * ez))] =
+                            in ? Material{1.0e4, 0.25} : Material{1.0, 0.3};
+                    }
+            break;
+        }
+        default:
+            throw ConfigError("make_config: config must be 1..5");
+    }
+    GeneratedProblem p = assemble_hex(mesh, mats);
+    if (cfg == 3) rhs = rhs_gaussian(p, derive_seed(base, 3));
+    else if (cfg == 4) rhs = rhs_top_pressure(p, 1.0);
+    else rhs = rhs_top_nodal(p, -1.0);
+    return p;
+}
+
+}  // namespace aspamg
