@@ -1,0 +1,416 @@
+#!/usr/bin/env python3
+"""Benchmark of the solve phase: PCG + aSP-AMG V(1,1)-cycle on one B200.
+
+A "step" is one full PCG solve (x0 = 0 -> ||r|| <= 1e-8 ||b||) of the
+BASELINE.json configs[1] workload (C2: 64^3 hex cube, 8^3-element blocks with
+log-uniform E in [1, 1e6], clamped z=0, top load) on the hierarchy produced
+once by the CPU setup and uploaded once. ``value`` is seconds per PCG
+iteration over the timed solves (inputs resident in HBM); ``ms_per_step`` is
+the time-to-1e-8. ``e2e`` is the same metric through the C-ABI call with host
+buffers (H2D of b, D2H of x and the residual history inside the timed region).
+
+``--impl reference`` times the reference's CPU path on the host cores: the
+restated pcg / vcycle_apply (oracle/oracle.c) driving the reference's own
+compiled spmv (oracle/_ref, sparse_matrix.cpp:96-107), each step a bounded
+sample of PCG iterations of the same workload.
+
+Multi-GPU (torchrun, N > 1): replicas only — every rank solves
+the same problem independently; times are the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import hashlib
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_DESC = {
+    1: "C1: 20^3 hex unit cube, E=1 nu=0.3, clamp z=0, top f_z=-1",
+    2: "C2: 64^3 hex unit cube, 8^3-element blocks E=10^(6u) nu=0.3, clamp z=0, top f_z=-1",
+    3: "C3: 96x96x24 box h=(1,1,0.05), interior nodes perturbed 0.3h, E=1 nu=0.3, clamp z=0, N(0,1) rhs",
+    4: "C4: 400x400x4 plate h=1, E=1 nu=0.49, clamped 4 sides, top pressure 1",
+    5: "C5: 128^3 cube, 200 spheres E=1e4 nu=0.25 in E=1 nu=0.3 matrix, clamp z=0, top f_z=-1",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Dist:
+    def __init__(self, ws, rank, local, backend):
+        self.ws, self.rank, self.local = ws, rank, local
+        self.pg = None
+        if ws > 1:
+            import torch
+            import torch.distributed as dist
+            if backend == "nccl":
+                torch.cuda.set_device(local)
+            dist.init_process_group(backend=backend)
+            self.dist = dist
+            self.torch = torch
+            self.backend = backend
+
+    def barrier(self):
+        if self.ws > 1:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.ws == 1:
+            return v
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.ws > 1:
+            self.dist.destroy_process_group()
+
+
+def file_hash(path):
+    h = hashlib.sha1()
+    with open(path, "rb") as f:
+        h.update(f.read())
+    return h.hexdigest()[:12]
+
+
+def get_hierarchy(P, cfg, scale, rank, dist, threads):
+    """CPU setup once (rank 0), cached on disk for the other ranks / reruns."""
+    from paper_1902_01715_b200 import _native as N
+    t0 = time.perf_counter()
+    prob = P.Problem.config(cfg, scale)
+    t_gen = time.perf_counter() - t0
+    cache_dir = os.path.join(ROOT, ".cache")
+    os.makedirs(cache_dir, exist_ok=True)
+    key = f"hier_c{cfg}_s{scale}_{file_hash(os.path.join(N.LIB_DIR, 'libaspamg_host.so'))}.bin"
+    path = os.path.join(cache_dir, key)
+    t_setup = None
+    if rank == 0 and not os.path.exists(path):
+        t0 = time.perf_counter()
+        h = P.Hierarchy.setup(prob.K, prob.coords, threads=threads)
+        t_setup = time.perf_counter() - t0
+        h.save(path + ".tmp")
+        os.replace(path + ".tmp", path)
+    dist.barrier()
+    if t_setup is None:
+        h = P.Hierarchy.load(path)
+        t_setup = h.info().T_p
+    return prob, h, t_gen, t_setup
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_reference_sample(h, rhs, threads, target_s=12.0, max_iters=60):
+    """Reference CPU path: restated pcg/vcycle on the reference's own spmv."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    use_ref = O.ref_available()
+    oh = O.OracleHierarchy(h, use_ref_spmv=use_ref, threads=threads)
+    t0 = time.perf_counter()
+    oh.pcg(rhs, rel_tol=0.0, max_it=2)
+    per_it = (time.perf_counter() - t0) / 2
+    iters = int(max(2, min(max_iters, target_s / max(per_it, 1e-6))))
+    return oh, use_ref, iters
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return 0
+    import paper_1902_01715_b200 as P
+
+    class _D:
+        def barrier(self):
+            pass
+
+    threads = os.cpu_count() or 1
+    prob, h, t_gen, t_setup = get_hierarchy(P, args.config, args.scale, 0, _D(), threads)
+    oh, use_ref, iters = cpu_reference_sample(h, prob.rhs, threads, target_s=args.ref_sample_s)
+    times, its = [], 0
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        st, x, hist, conv, trr = oh.pcg(prob.rhs, rel_tol=0.0, max_it=iters)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+            its += len(hist)
+    value = sum(times) / its
+    kind = "reference" if use_ref else "port"
+    sample = (f"{iters} PCG iterations per step (x0=0, same hierarchy as the GPU arm) of "
+              f"{'restated pcg/vcycle_apply (oracle/oracle.c) on the reference spmv compiled from sparse_matrix.cpp' if use_ref else 'the oracle port'}; "
+              f"full solve is ~{args.full_iters or 'n_it'} iterations")
+    line = {
+        "impl": "reference",
+        "metric": "PCG+AMG solve: s/iteration (time-to-1e-8 = s/it x n_it)",
+        "value": value, "unit": "s/iteration", "higher_is_better": False,
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_DESC[args.config], "n": prob.K.n_rows, "nnz": prob.K.nnz,
+                   "scale": args.scale, "setup_s": t_setup, "l2": "inputs larger than L2 (K alone > 126 MB)" if args.config != 1 else "K fits L2"},
+        "cpu_baseline": {"value": value, "unit": "s/iteration", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "s/iteration", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args, ws, rank, local):
+    import paper_1902_01715_b200 as P
+    from paper_1902_01715_b200 import _native as N
+    dist = Dist(ws, rank, local, "nccl")
+    threads = max(1, (os.cpu_count() or 1) // max(1, ws))
+    prob, h, t_gen, t_setup = get_hierarchy(P, args.config, args.scale, rank, dist, os.cpu_count() or 1)
+    info = h.info()
+    t0 = time.perf_counter()
+    g = P.GpuVcycle(h, device=local)
+    t_upload = time.perf_counter() - t0
+    lib = N.gpu()
+    n = prob.K.n_rows
+    nbytes = 8 * n
+    # device-resident inputs for the kernel-level value
+    b_dev = C.c_void_p()
+    x_dev = C.c_void_p()
+    g._chk(lib.aspamg_gpu_alloc_device(g._ctx, nbytes, C.byref(b_dev)))
+    g._chk(lib.aspamg_gpu_alloc_device(g._ctx, nbytes, C.byref(x_dev)))
+    rhs = np.ascontiguousarray(prob.rhs)
+    g._chk(lib.aspamg_gpu_memcpy(g._ctx, b_dev, rhs.ctypes.data_as(C.c_void_p), nbytes))
+    max_it = args.max_it
+    hist = np.empty(max_it)
+    n_it = C.c_int64()
+    conv = C.c_int()
+    trr = C.c_double()
+    Pd = C.POINTER(C.c_double)
+
+    def solve_dev():
+        code = lib.aspamg_gpu_pcg_device(g._ctx, b_dev, None, args.tol, max_it, x_dev, hist.ctypes.data_as(Pd),
+                                         C.byref(n_it), C.byref(conv), C.byref(trr))
+        if code not in (0, 6):
+            g._chk(code)
+        ms = C.c_double()
+        lib.aspamg_gpu_last_solve_ms(g._ctx, C.byref(ms))
+        lc = C.c_int64()
+        lib.aspamg_gpu_launch_count(g._ctx, C.byref(lc))
+        return ms.value, int(n_it.value), bool(conv.value), float(trr.value), int(lc.value)
+
+    for _ in range(args.warmup):
+        solve_dev()
+    dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    tot_ms, tot_it, launches = 0.0, 0, 0
+    per_solve = []
+    for _ in range(args.steps):
+        ms, it, cv, tr, lc = solve_dev()
+        tot_ms += ms
+        tot_it += it
+        launches += lc
+        per_solve.append((ms, it, cv, tr))
+    clocks = clk.stop()
+    dist.barrier()
+    tot_ms = dist.max(tot_ms)
+    value = (tot_ms / 1e3) / max(tot_it, 1)
+    n_iters = per_solve[-1][1]
+    converged = all(p[2] for p in per_solve)
+
+    # e2e through the public C-ABI with pinned host buffers (H2D b, D2H x + history)
+    pin_b = C.c_void_p()
+    pin_x = C.c_void_p()
+    pin_h = C.c_void_p()
+    lib.aspamg_gpu_alloc_pinned(nbytes, C.byref(pin_b))
+    lib.aspamg_gpu_alloc_pinned(nbytes, C.byref(pin_x))
+    lib.aspamg_gpu_alloc_pinned(8 * max_it, C.byref(pin_h))
+    C.memmove(pin_b, rhs.ctypes.data, nbytes)
+    e2e_t, e2e_it = 0.0, 0
+    bp = C.cast(pin_b, Pd)
+    xp = C.cast(pin_x, Pd)
+    hp = C.cast(pin_h, Pd)
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        code = lib.aspamg_gpu_pcg(g._ctx, bp, None, args.tol, max_it, xp, hp, C.byref(n_it), C.byref(conv),
+                                  C.byref(trr))
+        dt = time.perf_counter() - t0
+        if code not in (0, 6):
+            g._chk(code)
+        if s >= args.warmup:
+            e2e_t += dt
+            e2e_it += int(n_it.value)
+    e2e_t = dist.max(e2e_t)
+    e2e_value = e2e_t / max(e2e_it, 1)
+    x_host = np.ctypeslib.as_array(xp, shape=(n,)).copy()
+    lib.aspamg_gpu_free_pinned(pin_b)
+    lib.aspamg_gpu_free_pinned(pin_x)
+    lib.aspamg_gpu_free_pinned(pin_h)
+
+    # per-kernel breakdown of one iteration (events around each kernel, eager)
+    prof = g.profile_iteration()
+    vc = [p for p in prof if not p[0].startswith("pcg_")]
+    vc_ms = sum(p[2] for p in vc)
+    vc_bytes = sum(p[3] for p in vc)
+    it_ms = sum(p[2] for p in prof)
+    it_bytes = sum(p[3] for p in prof)
+    top = max(prof, key=lambda p: p[2])
+    name = top[0].split(".")[0]
+    k_ms, k_bytes = g.time_kernel(name, top[1], reps=args.kernel_reps)
+    peak, peak_kind = measured_peak()
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            traffic = tj.get(f"c{args.config}", {}).get(top[0])
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        oh, use_ref, iters = cpu_reference_sample(h, prob.rhs, os.cpu_count() or 1, target_s=args.ref_sample_s)
+        t0 = time.perf_counter()
+        oh.pcg(prob.rhs, rel_tol=0.0, max_it=iters)
+        dt = time.perf_counter() - t0
+        cpu = {"value": dt / iters, "unit": "s/iteration", "cores": os.cpu_count() or 1,
+               "kind": "reference" if use_ref else "port",
+               "sample": f"{iters} PCG iterations of this workload (same hierarchy), "
+                         f"{'restated pcg/vcycle on the reference spmv (oracle/_ref)' if use_ref else 'oracle port'}"}
+
+    dist.close()
+    if rank != 0:
+        return 0
+    lv0 = g.level_info(0)
+    line = {
+        "metric": "PCG+AMG solve: s/iteration (time-to-1e-8 = ms_per_step)",
+        "value": value, "unit": "s/iteration", "higher_is_better": False,
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_ms / args.steps, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_DESC[args.config], "n": n, "nnz": prob.K.nnz, "scale": args.scale,
+                   "levels": int(info.n_levels), "C_gd": info.C_gd, "C_op": info.C_op, "C_fs": info.C_fs,
+                   "n_it": n_iters, "converged": converged, "true_rel_res": per_solve[-1][3],
+                   "rel_tol": args.tol, "K_format": "bsr3" if lv0.a_format == 1 else "csr",
+                   "setup_s": t_setup, "upload_s": t_upload, "parallelism": f"replicas x{ws}",
+                   "l2": "inputs larger than L2 (K alone > 126 MB), no flush" if args.config != 1 else "K fits in L2"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": top[0], "level": top[1], "kernel_ms": k_ms,
+                     "alg_bytes": k_bytes, "peak_kind": peak_kind},
+        "vcycle": {"ms": vc_ms, "alg_bytes": vc_bytes, "gbs": vc_bytes / (vc_ms * 1e-3) / 1e9 if vc_ms else None,
+                   "frac": (vc_bytes / (vc_ms * 1e-3) / 1e9) / peak if vc_ms else None,
+                   "iteration_ms_eager": it_ms, "iteration_alg_bytes": it_bytes},
+        "kernels": [{"name": p[0], "level": p[1], "ms": round(p[2], 5), "gbs": round(p[3] / (p[2] * 1e-3) / 1e9, 1) if p[2] else None}
+                    for p in prof],
+        "e2e": {"value": e2e_value, "unit": "s/iteration", "h2d_bytes_per_step": nbytes,
+                "d2h_bytes_per_step": nbytes + 8 * n_iters},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "time_to_1e8_s": tot_ms / args.steps / 1e3,
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=int, default=1)
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--max-it", dest="max_it", type=int, default=1000)
+    ap.add_argument("--kernel-reps", dest="kernel_reps", type=int, default=20)
+    ap.add_argument("--ref-sample-s", dest="ref_sample_s", type=float, default=12.0)
+    ap.add_argument("--full-iters", dest="full_iters", type=int, default=0)
+    ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+    return run_b200(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

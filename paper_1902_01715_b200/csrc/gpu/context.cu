@@ -346,16 +346,21 @@ void ensure_ready(aspamg_gpu_ctx* c) {
     if (!c->finalized) throw Fail{4, "context not finalized (upload levels + coarse factor, then finalize)"};
 }
 
+cudaGraph_t capture(aspamg_gpu_ctx* c, const std::vector<Op>& ops) {
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    run_ops(ops, c->stream);
+    cudaGraph_t g = nullptr;
+    const cudaError_t le = cudaGetLastError();
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);  // always leave capture mode
+    CK(le);
+    CK(ce);
+    return g;
+}
+
 void build_graphs(aspamg_gpu_ctx* c) {
-    // standalone V-cycle graph
-    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    run_ops(c->vc_ops, c->stream);
-    CK(cudaStreamEndCapture(c->stream, &c->vc_graph));
+    c->vc_graph = capture(c, c->vc_ops);  // standalone V-cycle
     CK(cudaGraphInstantiate(&c->vc_exec, c->vc_graph, 0));
-    // PCG body graph (host-loop fallback)
-    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    run_ops(c->body, c->stream);
-    CK(cudaStreamEndCapture(c->stream, &c->body_graph));
+    c->body_graph = capture(c, c->body);  // PCG body (host-loop fallback)
     CK(cudaGraphInstantiate(&c->body_exec, c->body_graph, 0));
 }
 
@@ -375,21 +380,20 @@ void build_device_loop(aspamg_gpu_ctx* c) {
     cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
     // rebuild the body op list with the condition handle wired into pcg_xr
     const std::vector<Op>& body = c->body;
+    // pcg_xr with the conditional: its reduction site is allocated before capture
+    const int n = c->lv[0].n;
+    const int g = vec_grid(n);
+    Red red = make_red(c, g, FIN_RR);
+    red.cond = handle;
+    red.use_cond = 1;
     CK(cudaStreamBeginCaptureToGraph(c->stream, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     for (size_t i = 0; i + 1 < body.size(); ++i) body[i].fn(c->stream);
-    {
-        // pcg_xr with the conditional
-        const int n = c->lv[0].n;
-        const int g = vec_grid(n);
-        Red red = make_red(c, g, FIN_RR);
-        red.cond = handle;
-        red.use_cond = 1;
-        double *x = c->x, *r = c->r, *p = c->p, *q = c->q;
-        const int* done = &c->st->done;
-        pcg_xr(n, x, r, p, q, red, done, Launch{g, c->stream});
-    }
+    pcg_xr(n, c->x, c->r, c->p, c->q, red, &c->st->done, Launch{g, c->stream});
     cudaGraph_t out;
-    CK(cudaStreamEndCapture(c->stream, &out));
+    const cudaError_t le = cudaGetLastError();
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &out);
+    CK(le);
+    CK(ce);
     CK(cudaGraphInstantiate(&c->pcg_exec, c->pcg_graph, 0));
 }
 
@@ -711,6 +715,8 @@ int aspamg_gpu_upload_coarse(aspamg_gpu_ctx* c, int64_t n_c, const double* Lc) {
         CK(cudaMemcpy(c->Lcm, cm.data(), cm.size() * 8, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(c->Dinv_f, df.data(), df.size() * 8, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(c->Dinv_b, db.data(), db.size() * 8, cudaMemcpyHostToDevice));
+        coarse_prepare(n);
+        CK(cudaGetLastError());
         c->coarse_uploaded = true;
     });
 }

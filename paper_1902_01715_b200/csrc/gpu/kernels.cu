@@ -439,8 +439,12 @@ void coarse_solve(int n, const double* Lrm, const double* Lcm, const double* Din
                   const double* y, double* z, const double* dotw, const Red& red, const int* done,
                   const Launch& L) {
     const size_t smem = sizeof(double) * (size_t)(n > 0 ? n : 1);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_coarse<<<1, kCoarseThreads, smem, L.stream>>>(n, Lrm, Lcm, Dinv_f, Dinv_b, y, z, dotw, red, done);
+}
+
+void coarse_prepare(int n) {
+    const size_t smem = sizeof(double) * (size_t)(n > 0 ? n : 1);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 void fill_zero(int n, double* y, const int* done, const Launch& L) {

@@ -111,6 +111,7 @@ int vec_grid(int n);
 void coarse_solve(int n, const double* Lrm, const double* Lcm, const double* Dinv_f, const double* Dinv_b,
                   const double* y, double* z, const double* dotw, const Red& red, const int* done, const Launch& L);
 
+void coarse_prepare(int n);  // once per factor size, outside any stream capture
 void fill_zero(int n, double* y, const int* done, const Launch& L);
 
 }  // namespace aspamg_gpu

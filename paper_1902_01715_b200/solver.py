@@ -148,9 +148,12 @@ class Problem:
         return cls(h)
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            N.host().aspamg_problem_free(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                N.host().aspamg_problem_free(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 # ---------------------------------------------------------------- hierarchy
@@ -236,9 +239,12 @@ class Hierarchy:
         return np.ctypeslib.as_array(p, shape=(n.value * n.value,)).reshape(n.value, n.value, order="F").copy()
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            N.host().aspamg_hierarchy_free(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                N.host().aspamg_hierarchy_free(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 # ---------------------------------------------------------------- GPU solve

@@ -1,0 +1,75 @@
+"""The drop-in boundary: both C-ABI libraries load and export every symbol the
+headers in include/ declare; without a GPU the CUDA path fails loudly (no CPU
+fallback)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+INC = os.path.join(ROOT, "include")
+LIB = os.path.join(ROOT, "paper_1902_01715_b200", "lib")
+
+
+def declared(header):
+    txt = open(os.path.join(INC, header)).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(aspamg_[a-z0-9_]+)\s*\(", txt)))
+
+
+def exported(lib):
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True, check=True).stdout
+    return {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+
+
+@pytest.mark.parametrize("header,lib", [("aspamg_gpu.h", "libaspamg_gpu.so"), ("aspamg_host.h", "libaspamg_host.so")])
+def test_every_declared_symbol_is_exported(header, lib):
+    path = os.path.join(LIB, lib)
+    assert os.path.exists(path), f"{lib} not built"
+    C.CDLL(path)  # loads without a GPU
+    names = declared(header)
+    assert len(names) >= 10
+    missing = [n for n in names if n not in exported(path)]
+    assert not missing, missing
+
+
+def test_gpu_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", os.path.join(LIB, "libaspamg_gpu.so")],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_oracle_in_product_path():
+    """The product package never loads the oracle (test infrastructure)."""
+    pkg = os.path.join(ROOT, "paper_1902_01715_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cpp", ".cu", ".cuh", ".hpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "pyoracle" not in txt and "liboracle" not in txt and "orc_" not in txt, f
+
+
+def test_gpu_calls_fail_loudly_without_device(pkg):
+    from paper_1902_01715_b200 import _native as N
+    lib = N.gpu()
+    n = C.c_int()
+    assert lib.aspamg_gpu_device_count(C.byref(n)) == 0
+    if n.value > 0:
+        pytest.skip("a CUDA device is present")
+    ctx = C.c_void_p()
+    assert lib.aspamg_gpu_ctx_create(0, C.byref(ctx)) == 5
+    assert b"no CUDA device" in lib.aspamg_gpu_last_error(None)
+    p = pkg.Problem.hex_cube(2)
+    h = pkg.Hierarchy.setup(p.K, p.coords)
+    with pytest.raises(pkg.CudaError):
+        pkg.GpuVcycle(h)
+
+
+def test_null_context_is_config_error():
+    from paper_1902_01715_b200 import _native as N
+    lib = N.gpu()
+    assert lib.aspamg_gpu_finalize(None) == 4
+    assert lib.aspamg_gpu_vcycle(None, None, None) == 4

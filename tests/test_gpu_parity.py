@@ -1,0 +1,244 @@
+"""GPU-vs-oracle parity through the C-ABI (include/aspamg_gpu.h).
+
+The oracle (oracle/oracle.c) runs on the SAME hierarchy arrays the GPU
+receives, so every difference is kernel arithmetic (FMA contraction, tree
+reductions) — the north_star tolerances apply: PCG iteration count +-1,
+first-20 relative residuals within 1e-9 relative, final solution 1e-8.
+Per-product tolerances are written per test.
+"""
+import numpy as np
+import pytest
+
+from conftest import problem_and_hierarchy, rel_err
+
+pytestmark = pytest.mark.gpu
+
+RTOL_SPMV = 1e-13   # one fp64 product, different summation order
+RTOL_VCYCLE = 1e-11  # a whole V-cycle (several levels of products)
+
+
+def _gpu(pkg, h, **opt):
+    return pkg.GpuVcycle(h, device=0, options=opt or None)
+
+
+def _oracle(oracle, h):
+    return oracle.OracleHierarchy(h, use_ref_spmv=False, threads=4)
+
+
+@pytest.fixture(scope="module")
+def c1_ctx(pkg, oracle):
+    p, h = problem_and_hierarchy(1, 1)
+    return p, h, _gpu(pkg, h), _oracle(oracle, h)
+
+
+def test_k_is_bsr3_and_levels_uploaded(c1_ctx):
+    p, h, g, o = c1_ctx
+    info = g.level_info(0)
+    assert info.a_format == 1 and info.a_fill == 1.0
+    assert info.a_nnzb * 9 == p.K.nnz
+    assert h.n_levels >= 2
+
+
+@pytest.mark.parametrize("which", ["A", "G", "Gt", "P", "Pt"])
+def test_spmv_every_operand_every_level(c1_ctx, pkg, which):
+    p, h, g, o = c1_ctx
+    rng = np.random.default_rng(7)
+    wi = ["A", "G", "Gt", "P", "Pt"].index(which)
+    for l in range(h.n_levels - (0 if which == "A" else 1)):
+        m = getattr(h.level(l, copy=False), which)
+        x = rng.standard_normal(m.n_cols)
+        yg = g.spmv(l, wi, x)
+        yo = o.spmv(l, which, x)
+        # per-entry bound: |sum| error <= nnz_row * eps * sum|a_ij x_j|
+        absrow = np.abs(m.to_scipy()) @ np.abs(x)
+        assert np.all(np.abs(yg - yo) <= 1e-14 * absrow + 1e-300), (which, l)
+
+
+def test_spmv_identity_and_zero(c1_ctx):
+    p, h, g, o = c1_ctx
+    n = p.K.n_rows
+    assert np.array_equal(g.spmv(0, 0, np.zeros(n)), np.zeros(n))
+
+
+def test_smoothing_step_matches_oracle_and_fixed_point(c1_ctx):
+    p, h, g, o = c1_ctx
+    rng = np.random.default_rng(3)
+    n = p.K.n_rows
+    b = rng.standard_normal(n)
+    x = rng.standard_normal(n)
+    assert rel_err(g.smooth(0, b, x), o.smooth(0, b, x)) < 1e-12
+    # exact solution is a fixed point: b = A x -> x' = x
+    bx = o.spmv(0, "A", x)
+    assert rel_err(g.smooth(0, bx, x), x) < 1e-12
+
+
+def test_coarse_solve_matches_oracle(c1_ctx):
+    p, h, g, o = c1_ctx
+    rng = np.random.default_rng(5)
+    n_c = h.coarse_factor().shape[0]
+    y = rng.standard_normal(n_c)
+    zg = g.coarse_solve(y)
+    zo = o.coarse_solve(y)
+    assert rel_err(zg, zo) < 1e-10
+    # L L' z = y
+    L = h.coarse_factor()
+    assert rel_err(L @ (L.T @ zg), y) < 1e-10
+
+
+def test_vcycle_matches_oracle(c1_ctx):
+    p, h, g, o = c1_ctx
+    rng = np.random.default_rng(11)
+    for _ in range(3):
+        y = rng.standard_normal(p.K.n_rows)
+        assert rel_err(g.apply(y), o.vcycle(y)) < RTOL_VCYCLE
+    assert np.array_equal(g.apply(np.zeros(p.K.n_rows)), np.zeros(p.K.n_rows))
+
+
+def test_vcycle_symmetric_positive_definite(c1_ctx):
+    """<B^-1 u, v> = <u, B^-1 v> to 1e-10, <B^-1 u, u> > 0."""
+    p, h, g, o = c1_ctx
+    rng = np.random.default_rng(13)
+    for _ in range(5):
+        u = rng.standard_normal(p.K.n_rows)
+        v = rng.standard_normal(p.K.n_rows)
+        bu, bv = g.apply(u), g.apply(v)
+        assert abs(bu @ v - u @ bv) <= 1e-10 * max(abs(bu @ v), 1e-300)
+        assert bu @ u > 0
+
+
+def test_vcycle_is_deterministic(c1_ctx):
+    p, h, g, o = c1_ctx
+    y = np.random.default_rng(17).standard_normal(p.K.n_rows)
+    assert np.array_equal(g.apply(y), g.apply(y))
+
+
+def _pcg_parity(p, h, g, o, tol=1e-8, max_it=1000):
+    xg, rep = g.pcg(p.rhs, rel_tol=tol, max_it=max_it)
+    st, xo, ho, conv_o, trr_o = o.pcg(p.rhs, rel_tol=tol, max_it=max_it)
+    assert st == 0
+    assert rep.converged and conv_o
+    assert abs(rep.iterations - len(ho)) <= 1, (rep.iterations, len(ho))
+    k = min(20, rep.iterations, len(ho))
+    assert np.all(np.abs(rep.residual_history[:k] - ho[:k]) <= 1e-9 * ho[:k]), "first-20 residual history"
+    assert rel_err(xg, xo) <= 1e-8
+    assert rep.true_rel_residual <= 10 * tol
+    assert len(rep.residual_history) == rep.iterations
+    return rep, ho
+
+
+def test_pcg_c1_full_size(c1_ctx):
+    p, h, g, o = c1_ctx
+    rep, ho = _pcg_parity(p, h, g, o)
+    assert rep.iterations <= 120  # SPEC.md:657 acceptance #4 spirit
+
+
+def test_pcg_deterministic_and_repeatable(c1_ctx):
+    p, h, g, o = c1_ctx
+    x1, r1 = g.pcg(p.rhs)
+    x2, r2 = g.pcg(p.rhs)
+    assert np.array_equal(x1, x2) and np.array_equal(r1.residual_history, r2.residual_history)
+
+
+def test_pcg_host_loop_matches_device_loop(pkg, oracle):
+    p, h = problem_and_hierarchy(1, 2)
+    g1 = _gpu(pkg, h)
+    g2 = _gpu(pkg, h, device_loop=0)
+    x1, r1 = g1.pcg(p.rhs)
+    x2, r2 = g2.pcg(p.rhs)
+    assert r1.iterations == r2.iterations
+    assert np.array_equal(x1, x2)
+
+
+def test_pcg_with_x0_and_edge_cases(c1_ctx, pkg):
+    p, h, g, o = c1_ctx
+    n = p.K.n_rows
+    # b = 0 -> x = 0, 0 iterations
+    x, rep = g.pcg(np.zeros(n))
+    assert rep.iterations == 0 and rep.converged and not np.any(x)
+    # x0 = exact-ish solution -> 0 or few iterations
+    xs, _ = g.pcg(p.rhs)
+    x, rep = g.pcg(p.rhs, x0=xs)
+    assert rep.iterations <= 1
+    # random x0 agrees with the oracle
+    x0 = np.random.default_rng(1).standard_normal(n)
+    xg, rg = g.pcg(p.rhs, x0=x0)
+    st, xo, ho, conv, trr = o.pcg(p.rhs, x0=x0)
+    assert abs(rg.iterations - len(ho)) <= 1 and rel_err(xg, xo) < 1e-8
+    # max_it cap -> not converged, history length == max_it
+    x, rep = g.pcg(p.rhs, max_it=3)
+    assert rep.iterations == 3 and not rep.converged
+    # dimension mismatch -> DimensionError
+    with pytest.raises(pkg.DimensionError):
+        g.pcg(np.ones(n + 1))
+
+
+def test_pcg_not_spd_raises(pkg):
+    """p'Ap <= 0 -> NotSpdError: negate the operator."""
+    p, h = problem_and_hierarchy(1, 4)
+    import ctypes as C
+    from paper_1902_01715_b200 import _native as N
+    lib = N.gpu()
+    ctx = C.c_void_p()
+    assert lib.aspamg_gpu_ctx_create(0, C.byref(ctx)) == 0
+    info = h.info()
+    for l in range(info.n_levels):
+        lv = h.level(l)
+        if l == 0:
+            lv.A.values = -lv.A.values
+        views = [m.view() for m in (lv.A, lv.G, lv.Gt, lv.P, lv.Pt)]
+        assert lib.aspamg_gpu_upload_level(ctx, l, *[C.byref(v) for v in views], lv.omega if l < info.n_levels - 1 else 1.0) == 0
+    L = np.ascontiguousarray(h.coarse_factor().ravel(order="F"))
+    assert lib.aspamg_gpu_upload_coarse(ctx, h.coarse_factor().shape[0], L.ctypes.data_as(C.POINTER(C.c_double))) == 0
+    assert lib.aspamg_gpu_finalize(ctx) == 0
+    n = p.K.n_rows
+    b = np.ascontiguousarray(p.rhs)
+    x = np.empty(n)
+    hist = np.empty(100)
+    n_it = C.c_int64()
+    conv = C.c_int()
+    trr = C.c_double()
+    P_d = C.POINTER(C.c_double)
+    code = lib.aspamg_gpu_pcg(ctx, b.ctypes.data_as(P_d), None, 1e-8, 100, x.ctypes.data_as(P_d),
+                              hist.ctypes.data_as(P_d), C.byref(n_it), C.byref(conv), C.byref(trr))
+    assert code == 2
+    lib.aspamg_gpu_ctx_destroy(ctx)
+
+
+@pytest.mark.parametrize("cfg,scale", [(2, 4), (3, 4), (4, 8), (5, 8)])
+def test_pcg_configs_scaled(pkg, oracle, cfg, scale):
+    """Same construction as BASELINE configs 2-5 at reduced element counts."""
+    p, h = problem_and_hierarchy(cfg, scale)
+    g = _gpu(pkg, h)
+    o = _oracle(oracle, h)
+    _pcg_parity(p, h, g, o)
+
+
+def test_pcg_c2_full_size(pkg, oracle):
+    """BASELINE config 2 at full size (0.8M dofs, 63.7M nnz)."""
+    p, h = problem_and_hierarchy(2, 1)
+    g = _gpu(pkg, h)
+    o = oracle.OracleHierarchy(h, use_ref_spmv=False, threads=8)
+    _pcg_parity(p, h, g, o)
+
+
+def test_nu_variants_match_oracle(pkg, oracle):
+    p, h = problem_and_hierarchy(1, 2, nu1=2, nu2=1)
+    g = _gpu(pkg, h)
+    o = _oracle(oracle, h)
+    y = np.random.default_rng(2).standard_normal(p.K.n_rows)
+    assert rel_err(g.apply(y), o.vcycle(y)) < RTOL_VCYCLE
+    _pcg_parity(p, h, g, o)
+
+
+def test_one_level_hierarchy_is_direct_solve(pkg, oracle):
+    """n <= min_coarse_size -> the V-cycle is the exact solve."""
+    p = pkg.Problem.hex_cube(3)
+    h = pkg.Hierarchy.setup(p.K, p.coords)
+    assert h.n_levels == 1
+    g = _gpu(pkg, h)
+    y = np.random.default_rng(4).standard_normal(p.K.n_rows)
+    z = g.apply(y)
+    K = p.K.to_scipy()
+    assert rel_err(K @ z, y) < 1e-10
+    x, rep = g.pcg(p.rhs)
+    assert rep.iterations == 1 and rep.converged  # exact preconditioner
