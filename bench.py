@@ -358,6 +358,12 @@ def run_b200(args, ws, rank, local):
     if rank != 0:
         return 0
     lv0 = g.level_info(0)
+    fmts = {0: "csr", 1: "sbsr3", 2: "sell", -1: None}
+    levels = []
+    for l in range(int(info.n_levels)):
+        li = g.level_info(l)
+        levels.append({"n": int(li.n), "nnz_A": int(li.a_nnz), "fmt": [fmts[int(f)] for f in li.fmt],
+                       "fill": [round(float(f), 3) for f in li.fill], "omega": round(float(li.omega), 4)})
     line = {
         "metric": "PCG+AMG solve: s/iteration (time-to-1e-8 = ms_per_step)",
         "value": value, "unit": "s/iteration", "higher_is_better": False,
@@ -380,6 +386,7 @@ def run_b200(args, ws, rank, local):
                     for p in prof],
         "e2e": {"value": e2e_value, "unit": "s/iteration", "h2d_bytes_per_step": nbytes,
                 "d2h_bytes_per_step": nbytes + 8 * n_iters},
+        "levels": levels,
         "gpu_launches": launches,
         "clocks": clocks,
         "time_to_1e8_s": tot_ms / args.steps / 1e3,

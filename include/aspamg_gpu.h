@@ -43,13 +43,15 @@ typedef struct aspamg_gpu_ctx aspamg_gpu_ctx;
 
 typedef struct aspamg_gpu_level_stats {
     int64_t n;
-    int32_t a_format;     /* 0 CSR, 1 exact 3x3 BSR */
+    int32_t a_format;     /* 0 CSR warp-per-row, 1 sliced 3x3 BSR, 2 SELL-32 */
     int64_t a_nnz, a_nnzb;
     double a_fill;        /* stored values / true nnz (1.0 = exact) */
     int64_t g_nnz, p_nnz;
     double omega;
     double alg_bytes_A, alg_bytes_G, alg_bytes_Gt, alg_bytes_P, alg_bytes_Pt; /* one product each */
     double device_bytes;
+    int32_t fmt[5];       /* formats of A, G, G', P, P' (same codes as a_format) */
+    double fill[5];       /* stored slots / true nnz per operand (padding of sliced formats) */
 } aspamg_gpu_level_stats;
 
 typedef struct aspamg_gpu_kernel_time {

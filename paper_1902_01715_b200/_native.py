@@ -52,7 +52,8 @@ class GpuLevelInfo(C.Structure):
     _fields_ = [("n", i64), ("a_format", i32), ("a_nnz", i64), ("a_nnzb", i64), ("a_fill", dbl),
                 ("g_nnz", i64), ("p_nnz", i64), ("omega", dbl),
                 ("alg_bytes_A", dbl), ("alg_bytes_G", dbl), ("alg_bytes_Gt", dbl),
-                ("alg_bytes_P", dbl), ("alg_bytes_Pt", dbl), ("device_bytes", dbl)]
+                ("alg_bytes_P", dbl), ("alg_bytes_Pt", dbl), ("device_bytes", dbl),
+                ("fmt", i32 * 5), ("fill", dbl * 5)]
 
 
 class GpuKernelTime(C.Structure):

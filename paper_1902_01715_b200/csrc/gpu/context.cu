@@ -64,10 +64,12 @@ struct aspamg_gpu_ctx {
     // coarsest factor
     int n_c = 0;
     double *Lrm = nullptr, *Lcm = nullptr, *Dinv_f = nullptr, *Dinv_b = nullptr;
+    double *Wrm = nullptr, *Wt = nullptr, *cw = nullptr;  // W = L^{-1} (lower), W' (upper), temp
     bool coarse_uploaded = false;
     bool finalized = false;
     // options
-    int opt_bsr = 1, opt_device_loop = 1;
+    int opt_bsr = 1, opt_device_loop = 1, opt_coarse_mode = 1;
+    long long opt_sell_max_mean = 48;
     long long opt_stream_bytes = 48ll << 20;
     // PCG state and vectors
     PcgState* st = nullptr;       // device
@@ -196,38 +198,95 @@ int group_for(double mean) {
     return g;
 }
 
+// Chunk metadata of a sliced layout: rows (or block rows) in chunks of 32,
+// chunk width = longest row of the chunk.
+void slice_meta(const std::vector<int>& len, std::vector<int2>& meta, long long& slots) {
+    const int n = (int)len.size();
+    const int nch = (n + 31) / 32;
+    meta.resize((size_t)std::max(nch, 1));
+    slots = 0;
+    for (int ch = 0; ch < nch; ++ch) {
+        int w = 0;
+        for (int l = 0; l < 32 && ch * 32 + l < n; ++l) w = std::max(w, len[(size_t)ch * 32 + l]);
+        if (slots > (1ll << 31) / 288) throw Fail{4, "sliced layout exceeds int32 slot indexing"};
+        meta[(size_t)ch] = make_int2((int)slots, w);
+        slots += w;
+    }
+}
+
 DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     DMat M;
     const long long nnz = v.nnz;
     const bool bsr = allow_bsr && c->opt_bsr && exact_bsr3(v);
+    const double mean = v.n_rows ? double(nnz) / double(v.n_rows) : 0.0;
     if (bsr) {
         M.fmt = 1;
-        DBsr3& B = M.bsr;
+        DSbsr3& B = M.sb;
         B.nb = (int)(v.n_rows / 3);
         B.nbc = (int)(v.n_cols / 3);
         B.nnzb = nnz / 9;
-        std::vector<int> rp(B.nb + 1), ci((size_t)B.nnzb);
-        std::vector<double> val((size_t)nnz);
+        B.nchunks = (B.nb + 31) / 32;
+        std::vector<int> len((size_t)B.nb);
+        for (int br = 0; br < B.nb; ++br)
+            len[(size_t)br] = (int)((v.row_offsets[3 * (int64_t)br + 1] - v.row_offsets[3 * (int64_t)br]) / 3);
+        std::vector<int2> meta;
+        slice_meta(len, meta, B.slots);
+        std::vector<int> ci((size_t)B.slots * 32, 0);
+        std::vector<double> val((size_t)B.slots * 288, 0.0);
         for (int br = 0; br < B.nb; ++br) {
+            const int ch = br / 32, lane = br % 32;
+            const long long off = meta[(size_t)ch].x;
             const int64_t r0 = 3 * (int64_t)br;
-            const int64_t len = v.row_offsets[r0 + 1] - v.row_offsets[r0];
-            const int64_t b0 = v.row_offsets[r0] / 9;  // 9 values per block, block rows consecutive
-            rp[br] = (int)b0;
-            for (int64_t t = 0; t < len / 3; ++t) {
-                ci[(size_t)(b0 + t)] = (int)(v.col_indices[v.row_offsets[r0] + 3 * t] / 3);
+            for (int j = 0; j < len[(size_t)br]; ++j) {
+                ci[(size_t)((off + j) * 32 + lane)] = (int)(v.col_indices[v.row_offsets[r0] + 3 * j] / 3);
                 for (int r = 0; r < 3; ++r)
                     for (int cc = 0; cc < 3; ++cc)
-                        val[(size_t)(9 * (b0 + t) + 3 * r + cc)] = v.values[v.row_offsets[r0 + r] + 3 * t + cc];
+                        val[(size_t)(((off + j) * 9 + 3 * r + cc) * 32 + lane)] = v.values[v.row_offsets[r0 + r] + 3 * j + cc];
             }
         }
-        rp[B.nb] = (int)B.nnzb;
-        B.rp = dalloc<int>(c, rp.size());
+        B.len = dalloc<int>(c, len.size());
+        B.meta = dalloc<int2>(c, meta.size());
         B.ci = dalloc<int>(c, ci.size());
         B.v = dalloc<double>(c, val.size());
-        CK(cudaMemcpy(B.rp, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(B.len, len.data(), len.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(B.meta, meta.data(), meta.size() * sizeof(int2), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(B.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(B.v, val.data(), val.size() * sizeof(double), cudaMemcpyHostToDevice));
         B.stream = (long long)(76.0 * B.nnzb) > c->opt_stream_bytes;
+        return M;
+    }
+    if (mean <= (double)c->opt_sell_max_mean) {
+        M.fmt = 2;
+        DSell& S = M.sell;
+        S.n_rows = (int)v.n_rows;
+        S.n_cols = (int)v.n_cols;
+        S.nnz = nnz;
+        S.nchunks = (S.n_rows + 31) / 32;
+        std::vector<int> len((size_t)std::max<int64_t>(v.n_rows, 1), 0);
+        for (int64_t i = 0; i < v.n_rows; ++i) len[(size_t)i] = (int)(v.row_offsets[i + 1] - v.row_offsets[i]);
+        len.resize((size_t)v.n_rows);
+        std::vector<int2> meta;
+        slice_meta(len, meta, S.slots);
+        std::vector<int> ci((size_t)std::max<long long>(S.slots * 32, 1), 0);
+        std::vector<double> val(ci.size(), 0.0);
+        for (int64_t i = 0; i < v.n_rows; ++i) {
+            const long long off = meta[(size_t)(i / 32)].x;
+            const int lane = (int)(i % 32);
+            for (int64_t k = v.row_offsets[i]; k < v.row_offsets[i + 1]; ++k) {
+                const long long j = k - v.row_offsets[i];
+                ci[(size_t)((off + j) * 32 + lane)] = (int)v.col_indices[k];
+                val[(size_t)((off + j) * 32 + lane)] = v.values[k];
+            }
+        }
+        S.len = dalloc<int>(c, len.size());
+        S.meta = dalloc<int2>(c, meta.size());
+        S.ci = dalloc<int>(c, ci.size());
+        S.v = dalloc<double>(c, val.size());
+        if (!len.empty()) CK(cudaMemcpy(S.len, len.data(), len.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(S.meta, meta.data(), meta.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(S.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(S.v, val.data(), val.size() * sizeof(double), cudaMemcpyHostToDevice));
+        S.stream = (long long)(12.0 * nnz) > c->opt_stream_bytes;
         return M;
     }
     M.fmt = 0;
@@ -246,23 +305,32 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         CK(cudaMemcpy(A.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(A.v, v.values, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice));
     }
-    A.group = group_for(v.n_rows ? double(nnz) / double(v.n_rows) : 1.0);
+    A.group = group_for(mean);
     A.stream = (long long)(12.0 * nnz) > c->opt_stream_bytes;
     return M;
+}
+
+// Stored (padded) entries / true nnz of an operand.
+double fill_ratio(const DMat& M) {
+    if (M.fmt == 1) return M.sb.nnzb ? double(M.sb.slots) * 32.0 / double(M.sb.nnzb) : 1.0;
+    if (M.fmt == 2) return M.sell.nnz ? double(M.sell.slots) * 32.0 / double(M.sell.nnz) : 1.0;
+    return 1.0;
 }
 
 // Algorithmic bytes of one product y = M x: matrix arrays
 // once, x once, y once; padding never counted.
 double alg_bytes(const DMat& M) {
     if (M.fmt == 1) {
-        const double nnzb = double(M.bsr.nnzb);
-        return 72.0 * nnzb + 4.0 * nnzb + 4.0 * (M.bsr.nb + 1) + 8.0 * M.cols() + 8.0 * M.rows();
+        const double nnzb = double(M.sb.nnzb);
+        return 72.0 * nnzb + 4.0 * nnzb + 4.0 * (M.sb.nb + 1) + 8.0 * M.cols() + 8.0 * M.rows();
     }
-    const double nnz = double(M.csr.nnz);
-    return 8.0 * nnz + 4.0 * nnz + 4.0 * (M.csr.n_rows + 1) + 8.0 * M.cols() + 8.0 * M.rows();
+    const double nnz = double(M.fmt == 2 ? M.sell.nnz : M.csr.nnz);
+    return 8.0 * nnz + 4.0 * nnz + 4.0 * (M.rows() + 1) + 8.0 * M.cols() + 8.0 * M.rows();
 }
 
-std::string fmt_name(const DMat& M) { return M.fmt == 1 ? "bsr3" : "csr" + std::to_string(M.csr.group); }
+std::string fmt_name(const DMat& M) {
+    return M.fmt == 1 ? "sbsr3" : M.fmt == 2 ? "sell" : "csr" + std::to_string(M.csr.group);
+}
 
 void add_spmv(aspamg_gpu_ctx* c, std::vector<Op>& ops, const std::string& name, int level, const DMat& M, Epi epi,
               const double* x, double* y, const double* aux, double omega, const double* dotw, int fin,
@@ -288,10 +356,24 @@ void build_vcycle(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* 
     const bool top = k == 0;
     if (k == L - 1) {  // coarsest: forward/backward solve
         Red red;
-        if (top && fin0 != FIN_NONE) red = make_red(c, 1, fin0);
         const int n = c->n_c;
-        const double *Lrm = c->Lrm, *Lcm = c->Lcm, *Df = c->Dinv_f, *Db = c->Dinv_b;
         const double* dw = top ? dotw0 : nullptr;
+        if (c->opt_coarse_mode == 1) {
+            if (top && fin0 != FIN_NONE) red = make_red(c, trmv_grid(n), fin0);
+            const double *W = c->Wrm, *Wt = c->Wt;
+            double* w = c->cw;
+            const int g = trmv_grid(n);
+            const double bytes = 8.0 * double(n) * (n + 1) / 2 + 16.0 * n;
+            ops.push_back({"coarse_fwd", k, bytes, [=](cudaStream_t s) {
+                               trmv(n, false, W, y, w, nullptr, Red{}, done, Launch{g, s});
+                           }});
+            ops.push_back({"coarse_bwd", k, bytes + (dw ? 8.0 * n : 0.0), [=](cudaStream_t s) {
+                               trmv(n, true, Wt, w, z, dw, red, done, Launch{g, s});
+                           }});
+            return;
+        }
+        if (top && fin0 != FIN_NONE) red = make_red(c, 1, fin0);
+        const double *Lrm = c->Lrm, *Lcm = c->Lcm, *Df = c->Dinv_f, *Db = c->Dinv_b;
         const double bytes = 2.0 * (8.0 * double(n) * (n + 1) / 2 + 16.0 * n);
         ops.push_back({"coarse_solve", k, bytes, [=](cudaStream_t s) {
                            Launch Lc{1, s};
@@ -615,6 +697,8 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         if (k == "bsr") c->opt_bsr = (int)value;
         else if (k == "device_loop") c->opt_device_loop = (int)value;
         else if (k == "stream_bytes") c->opt_stream_bytes = value;
+        else if (k == "sell_max_mean") c->opt_sell_max_mean = value;
+        else if (k == "coarse_mode") c->opt_coarse_mode = (int)value;
         else throw Fail{4, "set_option: unknown key " + k};
     });
 }
@@ -706,7 +790,23 @@ int aspamg_gpu_upload_coarse(aspamg_gpu_ctx* c, int64_t n_c, const double* Lc) {
                     db[(size_t)b * 1024 + 32 * i + j] = inv[j][i];  // (L_b^{-1})' = (L_b')^{-1}
                 }
         }
+        // W = L^{-1}: column j solves L w = e_j (forward substitution from row j)
+        std::vector<double> W((size_t)n * n, 0.0), Wt((size_t)n * n, 0.0);
+        for (int j = 0; j < n; ++j) {
+            for (int i = j; i < n; ++i) {
+                double sacc = (i == j) ? 1.0 : 0.0;
+                for (int k = j; k < i; ++k) sacc -= rm[(size_t)i * n + k] * W[(size_t)k * n + j];
+                W[(size_t)i * n + j] = sacc / rm[(size_t)i * n + i];
+            }
+        }
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j <= i; ++j) Wt[(size_t)j * n + i] = W[(size_t)i * n + j];
         c->n_c = n;
+        c->Wrm = dalloc<double>(c, W.size());
+        c->Wt = dalloc<double>(c, Wt.size());
+        c->cw = dalloc<double>(c, (size_t)n);
+        CK(cudaMemcpy(c->Wrm, W.data(), W.size() * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->Wt, Wt.data(), Wt.size() * 8, cudaMemcpyHostToDevice));
         c->Lrm = dalloc<double>(c, rm.size());
         c->Lcm = dalloc<double>(c, cm.size());
         c->Dinv_f = dalloc<double>(c, df.size());
@@ -742,10 +842,10 @@ int aspamg_gpu_level_info(aspamg_gpu_ctx* c, int64_t level, aspamg_gpu_level_sta
         o->n = l.n;
         o->a_format = l.A.fmt;
         o->a_nnz = l.a_nnz;
-        o->a_nnzb = l.A.fmt == 1 ? l.A.bsr.nnzb : 0;
-        o->a_fill = l.A.fmt == 1 ? 9.0 * l.A.bsr.nnzb / std::max<double>(1.0, (double)l.a_nnz) : 1.0;
-        o->g_nnz = l.has_smoother ? l.G.csr.nnz : 0;
-        o->p_nnz = l.has_smoother ? l.P.csr.nnz : 0;
+        o->a_nnzb = l.A.fmt == 1 ? l.A.sb.nnzb : 0;
+        o->a_fill = fill_ratio(l.A);
+        o->g_nnz = l.has_smoother ? (l.G.fmt == 2 ? l.G.sell.nnz : l.G.csr.nnz) : 0;
+        o->p_nnz = l.has_smoother ? (l.P.fmt == 2 ? l.P.sell.nnz : l.P.csr.nnz) : 0;
         o->omega = l.omega;
         o->alg_bytes_A = alg_bytes(l.A);
         if (l.has_smoother) {
@@ -755,6 +855,12 @@ int aspamg_gpu_level_info(aspamg_gpu_ctx* c, int64_t level, aspamg_gpu_level_sta
             o->alg_bytes_Pt = alg_bytes(l.Pt);
         }
         o->device_bytes = (double)c->device_bytes;
+        const DMat* ms[5] = {&l.A, &l.G, &l.Gt, &l.P, &l.Pt};
+        for (int i = 0; i < 5; ++i) {
+            const bool present = i == 0 || l.has_smoother;
+            o->fmt[i] = present ? ms[i]->fmt : -1;
+            o->fill[i] = present ? fill_ratio(*ms[i]) : 0.0;
+        }
     });
 }
 
@@ -843,7 +949,13 @@ int aspamg_gpu_coarse_solve(aspamg_gpu_ctx* c, const double* y, double* z) {
         CK(cudaMalloc(&dy, bytes));
         CK(cudaMalloc(&dz, bytes));
         cudaMemcpyAsync(dy, y, bytes, cudaMemcpyHostToDevice, c->stream);
-        coarse_solve(c->n_c, c->Lrm, c->Lcm, c->Dinv_f, c->Dinv_b, dy, dz, nullptr, Red{}, nullptr, Launch{1, c->stream});
+        if (c->opt_coarse_mode == 1) {
+            trmv(c->n_c, false, c->Wrm, dy, c->cw, nullptr, Red{}, nullptr, Launch{0, c->stream});
+            trmv(c->n_c, true, c->Wt, c->cw, dz, nullptr, Red{}, nullptr, Launch{0, c->stream});
+        } else {
+            coarse_solve(c->n_c, c->Lrm, c->Lcm, c->Dinv_f, c->Dinv_b, dy, dz, nullptr, Red{}, nullptr,
+                         Launch{1, c->stream});
+        }
         cudaMemcpyAsync(z, dz, bytes, cudaMemcpyDeviceToHost, c->stream);
         cudaError_t e = cudaStreamSynchronize(c->stream);
         cudaFree(dy);

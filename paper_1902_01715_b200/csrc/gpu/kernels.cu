@@ -1,7 +1,8 @@
 // sm_100a kernels of the solve path (PCG + V(nu1,nu2)-cycle), fp64.
 //
 // Replaces, per SURVEY.md §2 kernel table:
-//   k_bsr3   <- spmv sparse_matrix.cpp:96-107 on K (exact 3x3 blocks)
+//   k_sbsr3  <- spmv sparse_matrix.cpp:96-107 on K (exact 3x3 blocks, sliced, lane per block row)
+//   k_sell   <- spmv on short-row operands (SELL-32, lane per row)
 //   k_csr    <- spmv / spmv_transpose sparse_matrix.cpp:96-124 on G, G', P, P', A_l
 //              (G', P' stored explicitly -> every product is a row gather)
 //   epilogues fuse the V-cycle vector updates (Alg. 2):
@@ -134,12 +135,14 @@ __device__ void reduce_finish2(double v, double v2, const Red& red) {
     }
 }
 
+// Epilogues are written with explicit _rn intrinsics (no FMA contraction) so
+// they round exactly like the oracle's separate multiply / add.
 __device__ __forceinline__ double epilogue(int epi, double s, const double* aux, int row, double omega) {
     switch (epi) {
-        case EPI_SCALE: return omega * s;
-        case EPI_RESID: return aux[row] - s;
-        case EPI_ADD: return aux[row] + s;
-        case EPI_ADDSCALE: return aux[row] + omega * s;
+        case EPI_SCALE: return __dmul_rn(omega, s);
+        case EPI_RESID: return __dsub_rn(aux[row], s);
+        case EPI_ADD: return __dadd_rn(aux[row], s);
+        case EPI_ADDSCALE: return __dadd_rn(aux[row], __dmul_rn(omega, s));
         default: return s;
     }
 }
@@ -192,14 +195,100 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
 }
 
-// --------------------------------------------------------------- BSR3 SpMV
-// One warp per block row. The block row's values are one contiguous run of
-// 9*nnzb doubles; lane l takes flat positions l, l+32, ... (perfectly
-// coalesced 256-B warp loads), tracking (block, entry) incrementally
-// (32 = 3*9 + 5), and accumulates into the block's row r = entry/3 with the
-// gathered x[3*col + entry%3]. Three fixed shuffle trees finish the rows.
+constexpr int SB_U = 3;    // block slots per load group (sliced BSR3)
+constexpr int SELL_U = 8;  // slots per load group (SELL-32)
+
+// ------------------------------------------------------- sliced BSR3 SpMV
+// One lane per block row (3 rows of K), 32 block rows per warp-chunk. Per
+// block slot the warp issues one 128-B column load and nine 256-B value loads
+// (all fully coalesced), then gathers x[3c..3c+2] (L1/L2-resident). The three
+// row sums run sequentially in ascending column order with separate multiply
+// and add — exactly the reference spmv's arithmetic (sparse_matrix.cpp:100-105),
+// so y is bit-identical to it.
 template <bool STREAM>
-__global__ void __launch_bounds__(kBlock) k_bsr3(DBsr3 M, int epi, const double* __restrict__ x, double* y,
+__global__ void __launch_bounds__(kBlock) k_sbsr3(DSbsr3 M, int epi, const double* __restrict__ x, double* y,
+                                                   const double* aux, double omega, const double* dotw, Red red,
+                                                   const int* done) {
+    if (is_done(done)) return;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * kBlock) >> 5;
+    double dacc = 0.0;
+    for (int ch = warp; ch < M.nchunks; ch += nwarps) {
+        const int br = ch * 32 + lane;
+        const bool act = br < M.nb;
+        const int len = act ? __ldg(M.len + br) : 0;
+        const int2 mw = __ldg(M.meta + ch);
+        const int* cp = M.ci + (long long)mw.x * 32 + lane;
+        const double* vp = M.v + (long long)mw.x * 288 + lane;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        // Groups of SB_U slots: every load of the group is issued (predicated,
+        // never for padding) before the first use, so each lane keeps
+        // 10*SB_U independent DRAM loads and then 3*SB_U gathers in flight.
+        for (int j0 = 0; j0 < mw.y; j0 += SB_U) {
+            int c[SB_U];
+            double v[SB_U][9];
+            double xv[SB_U][3];
+#pragma unroll
+            for (int u = 0; u < SB_U; ++u) {
+                const int j = j0 + u;
+                c[u] = 0;
+#pragma unroll
+                for (int e = 0; e < 9; ++e) v[u][e] = 0.0;
+                if (j < len) {
+                    c[u] = ld_mat<STREAM>(cp + 32 * j);
+                    const double* vj = vp + 288ll * j;
+#pragma unroll
+                    for (int e = 0; e < 9; ++e) v[u][e] = ld_mat<STREAM>(vj + 32 * e);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < SB_U; ++u) {
+                xv[u][0] = xv[u][1] = xv[u][2] = 0.0;
+                if (j0 + u < len) {
+                    xv[u][0] = __ldg(x + 3 * c[u]);
+                    xv[u][1] = __ldg(x + 3 * c[u] + 1);
+                    xv[u][2] = __ldg(x + 3 * c[u] + 2);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < SB_U; ++u) {
+                if (j0 + u < len) {
+                    a0 = __dadd_rn(a0, __dmul_rn(v[u][0], xv[u][0]));
+                    a0 = __dadd_rn(a0, __dmul_rn(v[u][1], xv[u][1]));
+                    a0 = __dadd_rn(a0, __dmul_rn(v[u][2], xv[u][2]));
+                    a1 = __dadd_rn(a1, __dmul_rn(v[u][3], xv[u][0]));
+                    a1 = __dadd_rn(a1, __dmul_rn(v[u][4], xv[u][1]));
+                    a1 = __dadd_rn(a1, __dmul_rn(v[u][5], xv[u][2]));
+                    a2 = __dadd_rn(a2, __dmul_rn(v[u][6], xv[u][0]));
+                    a2 = __dadd_rn(a2, __dmul_rn(v[u][7], xv[u][1]));
+                    a2 = __dadd_rn(a2, __dmul_rn(v[u][8], xv[u][2]));
+                }
+            }
+        }
+        if (act) {
+            const int r0 = 3 * br;
+            const double o0 = epilogue(epi, a0, aux, r0, omega);
+            const double o1 = epilogue(epi, a1, aux, r0 + 1, omega);
+            const double o2 = epilogue(epi, a2, aux, r0 + 2, omega);
+            y[r0] = o0;
+            y[r0 + 1] = o1;
+            y[r0 + 2] = o2;
+            if (dotw) {
+                dacc = fma(o0, dotw[r0], dacc);
+                dacc = fma(o1, dotw[r0 + 1], dacc);
+                dacc = fma(o2, dotw[r0 + 2], dacc);
+            }
+        }
+    }
+    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
+}
+
+// ----------------------------------------------------------- SELL-32 SpMV
+// One lane per row; slot-major layout (coalesced); sequential ascending-column
+// sum with separate multiply/add (bit-identical to the reference spmv).
+template <bool STREAM>
+__global__ void __launch_bounds__(kBlock) k_sell(DSell M, int epi, const double* __restrict__ x, double* y,
                                                   const double* aux, double omega, const double* dotw, Red red,
                                                   const int* done) {
     if (is_done(done)) return;
@@ -207,35 +296,61 @@ __global__ void __launch_bounds__(kBlock) k_bsr3(DBsr3 M, int epi, const double*
     const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * kBlock) >> 5;
     double dacc = 0.0;
-    for (int br = warp; br < M.nb; br += nwarps) {
-        const int b0 = __ldg(M.rp + br), b1 = __ldg(M.rp + br + 1);
-        const int nval = 9 * (b1 - b0);
-        const double* vb = M.v + 9ll * b0;
-        const int* cb = M.ci + b0;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-        int blk = lane / 9, e = lane - 9 * (lane / 9);
-#pragma unroll 4
-        for (int p = lane; p < nval; p += 32) {
-            const double v = ld_mat<STREAM>(vb + p);
-            const int c = ld_mat<STREAM>(cb + blk);
-            const int r = e >= 6 ? 2 : (e >= 3 ? 1 : 0);
-            const double xv = __ldg(x + 3 * c + (e - 3 * r));
-            if (r == 0) a0 = fma(v, xv, a0);
-            else if (r == 1) a1 = fma(v, xv, a1);
-            else a2 = fma(v, xv, a2);
-            blk += 3;
-            e += 5;
-            if (e >= 9) { e -= 9; blk += 1; }
+    for (int ch = warp; ch < M.nchunks; ch += nwarps) {
+        const int row = ch * 32 + lane;
+        const bool act = row < M.n_rows;
+        const int len = act ? __ldg(M.len + row) : 0;
+        const int2 mw = __ldg(M.meta + ch);
+        const long long base = (long long)mw.x * 32 + lane;
+        double s = 0.0;
+        for (int j0 = 0; j0 < mw.y; j0 += SELL_U) {
+            double v[SELL_U], xv[SELL_U];
+            int c[SELL_U];
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u) {
+                v[u] = 0.0;
+                c[u] = 0;
+                if (j0 + u < len) {
+                    v[u] = ld_mat<STREAM>(M.v + base + 32ll * (j0 + u));
+                    c[u] = ld_mat<STREAM>(M.ci + base + 32ll * (j0 + u));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u) xv[u] = (j0 + u < len) ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u)
+                if (j0 + u < len) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
         }
-        a0 = warp_sum(a0);
-        a1 = warp_sum(a1);
-        a2 = warp_sum(a2);
-        if (lane < 3) {
-            const double s = lane == 0 ? a0 : (lane == 1 ? a1 : a2);
-            const int row = 3 * br + lane;
+        if (act) {
             const double out = epilogue(epi, s, aux, row, omega);
             y[row] = out;
             if (dotw) dacc = fma(out, dotw[row], dacc);
+        }
+    }
+    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
+}
+
+// ------------------------------------------------ dense triangular mat-vec
+// y = W x for W lower (row i: j <= i) or upper (row i: j >= i) stored dense
+// row-major; one warp per row, lane-strided coalesced loads, fixed tree sum.
+__global__ void __launch_bounds__(kBlock) k_trmv(int n, int upper, const double* __restrict__ W,
+                                                  const double* __restrict__ x, double* y, const double* dotw,
+                                                  Red red, const int* done) {
+    if (is_done(done)) return;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * kBlock) >> 5;
+    double dacc = 0.0;
+    for (int i = warp; i < n; i += nwarps) {
+        const double* row = W + (long long)i * n;
+        const int j0 = upper ? i : 0, j1 = upper ? n : i + 1;
+        double s = 0.0;
+#pragma unroll 4
+        for (int j = j0 + lane; j < j1; j += 32) s = fma(__ldg(row + j), __ldg(x + j), s);
+        s = warp_sum(s);
+        if (lane == 0) {
+            y[i] = s;
+            if (dotw) dacc = fma(s, dotw[i], dacc);
         }
     }
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
@@ -308,17 +423,19 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse(int n, const double* 
     for (int jb = 0; jb < nb; ++jb) {
         const int j0 = 32 * jb, bs = min(32, n - j0);
         if (w == 0) {
-            const double* D = Dinv_f + 1024ll * jb;
+            const double* D = Dinv_f + 1024ll * jb + 32 * lane;
             double acc = 0.0;
-            if (lane < bs)
-                for (int j = 0; j <= lane; ++j) acc = fma(D[32 * lane + j], zs[j0 + j], acc);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j <= lane && lane < bs) acc = fma(__ldg(D + j), zs[j0 + j], acc);
             __syncwarp();
             if (lane < bs) zs[j0 + lane] = acc;
         }
         __syncthreads();
         const double zl = lane < bs ? zs[j0 + lane] : 0.0;
+#pragma unroll 4
         for (int i = j0 + bs + w; i < n; i += nw) {
-            double t = lane < bs ? Lrm[(long long)i * n + j0 + lane] * zl : 0.0;
+            double t = lane < bs ? __ldg(Lrm + (long long)i * n + j0 + lane) * zl : 0.0;
             t = warp_sum(t);
             if (lane == 0) zs[i] -= t;
         }
@@ -328,17 +445,19 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse(int n, const double* 
     for (int jb = nb - 1; jb >= 0; --jb) {
         const int j0 = 32 * jb, bs = min(32, n - j0);
         if (w == 0) {
-            const double* D = Dinv_b + 1024ll * jb;
+            const double* D = Dinv_b + 1024ll * jb + 32 * lane;
             double acc = 0.0;
-            if (lane < bs)
-                for (int j = lane; j < bs; ++j) acc = fma(D[32 * lane + j], zs[j0 + j], acc);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j >= lane && j < bs && lane < bs) acc = fma(__ldg(D + j), zs[j0 + j], acc);
             __syncwarp();
             if (lane < bs) zs[j0 + lane] = acc;
         }
         __syncthreads();
         const double zl = lane < bs ? zs[j0 + lane] : 0.0;
+#pragma unroll 4
         for (int i = w; i < j0; i += nw) {
-            double t = lane < bs ? Lcm[(long long)i * n + j0 + lane] * zl : 0.0;
+            double t = lane < bs ? __ldg(Lcm + (long long)i * n + j0 + lane) * zl : 0.0;
             t = warp_sum(t);
             if (lane == 0) zs[i] -= t;
         }
@@ -380,8 +499,12 @@ int occ_grid(K kern, long long work_units_per_cta_needed) {
 // ------------------------------------------------------------------ host API
 int spmv_grid(const DMat& M) {
     if (M.fmt == 1) {
-        const long long warps = M.bsr.nb;
-        return M.bsr.stream ? occ_grid(k_bsr3<true>, (warps + 7) / 8) : occ_grid(k_bsr3<false>, (warps + 7) / 8);
+        const long long ch = M.sb.nchunks;
+        return M.sb.stream ? occ_grid(k_sbsr3<true>, (ch + 7) / 8) : occ_grid(k_sbsr3<false>, (ch + 7) / 8);
+    }
+    if (M.fmt == 2) {
+        const long long ch = M.sell.nchunks;
+        return M.sell.stream ? occ_grid(k_sell<true>, (ch + 7) / 8) : occ_grid(k_sell<false>, (ch + 7) / 8);
     }
     const int G = M.csr.group;
     const long long warps = ((long long)M.csr.n_rows * G + 31) / 32;
@@ -392,10 +515,17 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
           const Red& red, const int* done, const Launch& L) {
     const int grid = L.grid > 0 ? L.grid : spmv_grid(M);
     if (M.fmt == 1) {
-        if (M.bsr.stream)
-            k_bsr3<true><<<grid, kBlock, 0, L.stream>>>(M.bsr, epi, x, y, aux, omega, dotw, red, done);
+        if (M.sb.stream)
+            k_sbsr3<true><<<grid, kBlock, 0, L.stream>>>(M.sb, epi, x, y, aux, omega, dotw, red, done);
         else
-            k_bsr3<false><<<grid, kBlock, 0, L.stream>>>(M.bsr, epi, x, y, aux, omega, dotw, red, done);
+            k_sbsr3<false><<<grid, kBlock, 0, L.stream>>>(M.sb, epi, x, y, aux, omega, dotw, red, done);
+        return;
+    }
+    if (M.fmt == 2) {
+        if (M.sell.stream)
+            k_sell<true><<<grid, kBlock, 0, L.stream>>>(M.sell, epi, x, y, aux, omega, dotw, red, done);
+        else
+            k_sell<false><<<grid, kBlock, 0, L.stream>>>(M.sell, epi, x, y, aux, omega, dotw, red, done);
         return;
     }
 #define ASPAMG_CSR_CASE(GG)                                                                                   \
@@ -440,6 +570,13 @@ void coarse_solve(int n, const double* Lrm, const double* Lcm, const double* Din
                   const Launch& L) {
     const size_t smem = sizeof(double) * (size_t)(n > 0 ? n : 1);
     k_coarse<<<1, kCoarseThreads, smem, L.stream>>>(n, Lrm, Lcm, Dinv_f, Dinv_b, y, z, dotw, red, done);
+}
+
+int trmv_grid(int n) { return occ_grid(k_trmv, ((long long)n + 7) / 8); }
+
+void trmv(int n, bool upper, const double* W, const double* x, double* y, const double* dotw, const Red& red,
+          const int* done, const Launch& L) {
+    k_trmv<<<L.grid > 0 ? L.grid : trmv_grid(n), kBlock, 0, L.stream>>>(n, upper ? 1 : 0, W, x, y, dotw, red, done);
 }
 
 void coarse_prepare(int n) {

@@ -25,24 +25,47 @@ struct DCsr {
     bool stream = false;  // evict-first loads (matrix larger than ~L2/2)
 };
 
-// Exact 3x3 block CSR: nb block rows, values block-major (9 per block,
-// row-major inside the block), one int32 block column per block.
-struct DBsr3 {
-    int nb = 0, nbc = 0;
-    long long nnzb = 0;
-    int* rp = nullptr;
+// Sliced 3x3-block format for an exactly 3x3-blocked operator (K): block
+// rows are grouped in chunks of 32, one lane per block row. Chunk c has
+// width[c] block slots (the longest block row of the chunk) starting at slot
+// off[c]; slot j of lane l holds block column ci[(off+j)*32 + l] and the
+// block's 9 values (row-major) at v[((off+j)*9 + e)*32 + l]. Every warp load
+// is a contiguous 256-B (values) / 128-B (columns) line; each lane sums its
+// three rows sequentially in ascending column order (the reference's order,
+// sparse_matrix.cpp:100-105). Block rows shorter than the chunk width are
+// padded; padded slots are predicated off (never loaded).
+struct DSbsr3 {
+    int nb = 0, nbc = 0, nchunks = 0;
+    long long nnzb = 0, slots = 0;  // slots = padded block slots (incl. padding), per lane x 32
+    int* len = nullptr;             // blocks per block row
+    int2* meta = nullptr;           // per chunk {off, width}
     int* ci = nullptr;
     double* v = nullptr;
     bool stream = false;
 };
 
-// One matrix operand: BSR3 when the CSR is exactly 3x3-blocked, else CSR.
+// SELL-32 (sliced ELL, chunk height 32, no sorting): one lane per row,
+// same slot-major layout as DSbsr3 with scalar entries. Used for short rows
+// (G, G', P, P', short coarse A_l): coalesced, no cross-lane reduction,
+// sequential ascending-column sums.
+struct DSell {
+    int n_rows = 0, n_cols = 0, nchunks = 0;
+    long long nnz = 0, slots = 0;
+    int* len = nullptr;
+    int2* meta = nullptr;
+    int* ci = nullptr;
+    double* v = nullptr;
+    bool stream = false;
+};
+
+// One matrix operand.
 struct DMat {
-    int fmt = 0;  // 0 CSR, 1 BSR3
+    int fmt = 0;  // 0 CSR (group per row), 1 sliced BSR3, 2 SELL-32
     DCsr csr;
-    DBsr3 bsr;
-    int rows() const { return fmt == 1 ? 3 * bsr.nb : csr.n_rows; }
-    int cols() const { return fmt == 1 ? 3 * bsr.nbc : csr.n_cols; }
+    DSbsr3 sb;
+    DSell sell;
+    int rows() const { return fmt == 1 ? 3 * sb.nb : fmt == 2 ? sell.n_rows : csr.n_rows; }
+    int cols() const { return fmt == 1 ? 3 * sb.nbc : fmt == 2 ? sell.n_cols : csr.n_cols; }
 };
 
 // Epilogue of y = f(M x):
@@ -105,11 +128,18 @@ void pcg_xr(int n, double* x, double* r, const double* p, const double* q, const
 void pcg_init_dots(int n, const double* b, const double* r, const Red& red, const Launch& L);
 int vec_grid(int n);
 
-// Coarsest level: L L' z = y by blocked substitution (one CTA). Lrm: row-major
-// lower factor; Lcm: column-major (= row-major L'); Dinv: inverted 32x32
-// diagonal blocks (row-major, per block). Optional dot z.dotw -> red.
+// Coarsest level, "forward and backward solve" L L' z = y.
+// mode 0: blocked substitution in one CTA (Lrm row-major L, Lcm row-major L',
+//         Dinv_f / Dinv_b inverted 32x32 diagonal blocks).
+// mode 1: the two triangular solves applied through the explicit inverse
+//         factor W = L^{-1} (computed once at upload): w = W y, z = W' w, each a
+//         multi-CTA warp-per-row triangular mat-vec (Wrm: row-major W, lower;
+//         Wt: row-major W', upper).
 void coarse_solve(int n, const double* Lrm, const double* Lcm, const double* Dinv_f, const double* Dinv_b,
                   const double* y, double* z, const double* dotw, const Red& red, const int* done, const Launch& L);
+void trmv(int n, bool upper, const double* Wrm, const double* x, double* y, const double* dotw, const Red& red,
+          const int* done, const Launch& L);
+int trmv_grid(int n);
 
 void coarse_prepare(int n);  // once per factor size, outside any stream capture
 void fill_zero(int n, double* y, const int* done, const Launch& L);
