@@ -69,7 +69,8 @@ struct aspamg_gpu_ctx {
     bool finalized = false;
     // options
     int opt_bsr = 1, opt_device_loop = 1, opt_coarse_mode = 1;
-    long long opt_sell_max_mean = 48;
+    long long opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
+              opt_sell_u = 0;
     long long opt_stream_bytes = 48ll << 20;
     // PCG state and vectors
     PcgState* st = nullptr;       // device
@@ -192,9 +193,12 @@ void check_view(const aspamg_csr_view* v, const char* what) {
             throw Fail{1, std::string(what) + ": column index out of range"};
 }
 
-int group_for(double mean) {
+// Threads per row for the CSR kernel: ~4+ entries per thread, widened for
+// small levels so the grid still covers the GPU (>= ~150k threads).
+int group_for(double mean, int64_t n_rows) {
     int g = 1;
-    while (g < 32 && 2.0 * g <= mean) g *= 2;
+    while (g < 256 && 4.0 * 2 * g <= mean) g *= 2;
+    while (g < 256 && (double)n_rows * g < 150000.0 && 2.0 * g <= mean) g *= 2;
     return g;
 }
 
@@ -255,38 +259,63 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         B.stream = (long long)(76.0 * B.nnzb) > c->opt_stream_bytes;
         return M;
     }
-    if (mean <= (double)c->opt_sell_max_mean) {
+    std::vector<int> len((size_t)std::max<int64_t>(v.n_rows, 0), 0);
+    int maxlen = 0;
+    for (int64_t i = 0; i < v.n_rows; ++i) {
+        len[(size_t)i] = (int)(v.row_offsets[i + 1] - v.row_offsets[i]);
+        maxlen = std::max(maxlen, len[(size_t)i]);
+    }
+    if (v.n_rows > 0 && mean <= (double)c->opt_sell_max_mean && maxlen <= c->opt_sell_max_len) {
         M.fmt = 2;
         DSell& S = M.sell;
         S.n_rows = (int)v.n_rows;
         S.n_cols = (int)v.n_cols;
         S.nnz = nnz;
         S.nchunks = (S.n_rows + 31) / 32;
-        std::vector<int> len((size_t)std::max<int64_t>(v.n_rows, 1), 0);
-        for (int64_t i = 0; i < v.n_rows; ++i) len[(size_t)i] = (int)(v.row_offsets[i + 1] - v.row_offsets[i]);
-        len.resize((size_t)v.n_rows);
         std::vector<int2> meta;
         slice_meta(len, meta, S.slots);
+        // SELL-32-sigma: rows sorted by length (descending, stable) inside windows of
+        // sigma rows when the natural order pads too much.
+        std::vector<int> perm;
+        std::vector<int> slen = len;
+        if (nnz > 0 && double(S.slots) * 32.0 / double(nnz) > (double)c->opt_sell_sort_fill_pct / 100.0) {
+            const int64_t sigma = std::max<int64_t>(32, c->opt_sell_sigma);
+            perm.resize((size_t)v.n_rows);
+            for (int64_t i = 0; i < v.n_rows; ++i) perm[(size_t)i] = (int)i;
+            for (int64_t w0 = 0; w0 < v.n_rows; w0 += sigma) {
+                const int64_t w1 = std::min<int64_t>(v.n_rows, w0 + sigma);
+                std::stable_sort(perm.begin() + w0, perm.begin() + w1,
+                                 [&](int a, int b) { return len[(size_t)a] > len[(size_t)b]; });
+            }
+            for (int64_t i = 0; i < v.n_rows; ++i) slen[(size_t)i] = len[(size_t)perm[(size_t)i]];
+            slice_meta(slen, meta, S.slots);
+        }
         std::vector<int> ci((size_t)std::max<long long>(S.slots * 32, 1), 0);
         std::vector<double> val(ci.size(), 0.0);
-        for (int64_t i = 0; i < v.n_rows; ++i) {
-            const long long off = meta[(size_t)(i / 32)].x;
-            const int lane = (int)(i % 32);
+        for (int64_t sr = 0; sr < v.n_rows; ++sr) {
+            const int64_t i = perm.empty() ? sr : perm[(size_t)sr];
+            const long long off = meta[(size_t)(sr / 32)].x;
+            const int lane = (int)(sr % 32);
             for (int64_t k = v.row_offsets[i]; k < v.row_offsets[i + 1]; ++k) {
                 const long long j = k - v.row_offsets[i];
                 ci[(size_t)((off + j) * 32 + lane)] = (int)v.col_indices[k];
                 val[(size_t)((off + j) * 32 + lane)] = v.values[k];
             }
         }
-        S.len = dalloc<int>(c, len.size());
+        S.len = dalloc<int>(c, slen.size());
         S.meta = dalloc<int2>(c, meta.size());
         S.ci = dalloc<int>(c, ci.size());
         S.v = dalloc<double>(c, val.size());
-        if (!len.empty()) CK(cudaMemcpy(S.len, len.data(), len.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(S.len, slen.data(), slen.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(S.meta, meta.data(), meta.size() * sizeof(int2), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(S.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(S.v, val.data(), val.size() * sizeof(double), cudaMemcpyHostToDevice));
+        if (!perm.empty()) {
+            S.perm = dalloc<int>(c, perm.size());
+            CK(cudaMemcpy(S.perm, perm.data(), perm.size() * sizeof(int), cudaMemcpyHostToDevice));
+        }
         S.stream = (long long)(12.0 * nnz) > c->opt_stream_bytes;
+        S.u = c->opt_sell_u > 0 ? (int)c->opt_sell_u : (maxlen <= 4 ? 4 : 8);
         return M;
     }
     M.fmt = 0;
@@ -305,7 +334,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         CK(cudaMemcpy(A.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(A.v, v.values, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice));
     }
-    A.group = group_for(mean);
+    A.group = group_for(mean, v.n_rows);
     A.stream = (long long)(12.0 * nnz) > c->opt_stream_bytes;
     return M;
 }
@@ -329,7 +358,7 @@ double alg_bytes(const DMat& M) {
 }
 
 std::string fmt_name(const DMat& M) {
-    return M.fmt == 1 ? "sbsr3" : M.fmt == 2 ? "sell" : "csr" + std::to_string(M.csr.group);
+    return M.fmt == 1 ? "sbsr3" : M.fmt == 2 ? (M.sell.perm ? "sells" : "sell") : "csr" + std::to_string(M.csr.group);
 }
 
 void add_spmv(aspamg_gpu_ctx* c, std::vector<Op>& ops, const std::string& name, int level, const DMat& M, Epi epi,
@@ -698,6 +727,10 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "device_loop") c->opt_device_loop = (int)value;
         else if (k == "stream_bytes") c->opt_stream_bytes = value;
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;
+        else if (k == "sell_max_len") c->opt_sell_max_len = value;
+        else if (k == "sell_sigma") c->opt_sell_sigma = value;
+        else if (k == "sell_sort_fill_pct") c->opt_sell_sort_fill_pct = value;
+        else if (k == "sell_u") c->opt_sell_u = value;
         else if (k == "coarse_mode") c->opt_coarse_mode = (int)value;
         else throw Fail{4, "set_option: unknown key " + k};
     });

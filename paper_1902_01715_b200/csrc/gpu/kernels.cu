@@ -158,35 +158,63 @@ __device__ __forceinline__ bool is_done(const int* done) {
 }
 
 // ---------------------------------------------------------------- CSR SpMV
-// G threads per row (warp-uniform loop so sub-warp shuffles stay converged);
-// each lane sums its strided entries in ascending order, then a fixed
-// shuffle tree. Loads of values/columns are coalesced across the group.
-template <int G, bool STREAM>
+// T threads per row (power of two, 1..256); a CTA owns 256/T consecutive rows
+// per step (CTA-uniform loop, so barriers are legal). Each thread walks its
+// strided entries in groups of CSR_U predicated loads issued before use, then
+// a fixed shuffle tree (and, for T > 32, a fixed smem combine of the warp sums).
+constexpr int CSR_U = 4;
+
+template <int T, bool STREAM>
 __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* __restrict__ x, double* y,
                                                  const double* aux, double omega, const double* dotw, Red red,
                                                  const int* done) {
     if (is_done(done)) return;
-    constexpr int GPW = 32 / G;
+    constexpr int RPC = kBlock / T;  // rows per CTA step
+    __shared__ double wsum[kBlock / 32];
+    const int t = threadIdx.x % T;
+    const int lr = threadIdx.x / T;
     const int lane = threadIdx.x & 31;
-    const int gl = lane % G, gw = lane / G;
-    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * kBlock) >> 5;
     double dacc = 0.0;
-    for (int base = warp * GPW; base < M.n_rows; base += nwarps * GPW) {
-        const int row = base + gw;
+    for (int rbase = blockIdx.x * RPC; rbase < M.n_rows; rbase += gridDim.x * RPC) {
+        const int row = rbase + lr;
         double s = 0.0;
         if (row < M.n_rows) {
             const int b = __ldg(M.rp + row), e = __ldg(M.rp + row + 1);
-#pragma unroll 4
-            for (int k = b + gl; k < e; k += G) {
-                const double v = ld_mat<STREAM>(M.v + k);
-                const int c = ld_mat<STREAM>(M.ci + k);
-                s = fma(v, __ldg(x + c), s);
+            for (int k0 = b + t; k0 < e; k0 += T * CSR_U) {
+                double v[CSR_U], xv[CSR_U];
+                int c[CSR_U];
+#pragma unroll
+                for (int u = 0; u < CSR_U; ++u) {
+                    const int k = k0 + u * T;
+                    v[u] = 0.0;
+                    c[u] = 0;
+                    if (k < e) {
+                        v[u] = ld_mat<STREAM>(M.v + k);
+                        c[u] = ld_mat<STREAM>(M.ci + k);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < CSR_U; ++u) xv[u] = (k0 + u * T < e) ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < CSR_U; ++u) s = fma(v[u], xv[u], s);
             }
         }
+        if constexpr (T <= 32) {
 #pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, G);
-        if (gl == 0 && row < M.n_rows) {
+            for (int o = T / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, T);
+        } else {
+            s = warp_sum(s);
+            if (lane == 0) wsum[threadIdx.x >> 5] = s;
+            __syncthreads();
+            if (t == 0) {
+                double a = 0.0;
+#pragma unroll
+                for (int w = 0; w < T / 32; ++w) a += wsum[(threadIdx.x >> 5) + w];
+                s = a;
+            }
+            __syncthreads();
+        }
+        if (t == 0 && row < M.n_rows) {
             const double out = epilogue(epi, s, aux, row, omega);
             y[row] = out;
             if (dotw) dacc = fma(out, dotw[row], dacc);
@@ -196,7 +224,6 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
 }
 
 constexpr int SB_U = 3;    // block slots per load group (sliced BSR3)
-constexpr int SELL_U = 8;  // slots per load group (SELL-32)
 
 // ------------------------------------------------------- sliced BSR3 SpMV
 // One lane per block row (3 rows of K), 32 block rows per warp-chunk. Per
@@ -286,8 +313,10 @@ __global__ void __launch_bounds__(kBlock) k_sbsr3(DSbsr3 M, int epi, const doubl
 
 // ----------------------------------------------------------- SELL-32 SpMV
 // One lane per row; slot-major layout (coalesced); sequential ascending-column
-// sum with separate multiply/add (bit-identical to the reference spmv).
-template <bool STREAM>
+// sum with separate multiply/add (bit-identical to the reference spmv). The
+// epilogue operands (aux, dotw) are fetched with the first load group so the
+// chunk costs ~2 dependent memory round trips (values/columns, then x).
+template <int U, bool STREAM>
 __global__ void __launch_bounds__(kBlock) k_sell(DSell M, int epi, const double* __restrict__ x, double* y,
                                                   const double* aux, double omega, const double* dotw, Red red,
                                                   const int* done) {
@@ -295,19 +324,23 @@ __global__ void __launch_bounds__(kBlock) k_sell(DSell M, int epi, const double*
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * kBlock) >> 5;
+    const bool need_aux = epi == EPI_RESID || epi == EPI_ADD || epi == EPI_ADDSCALE;
     double dacc = 0.0;
     for (int ch = warp; ch < M.nchunks; ch += nwarps) {
-        const int row = ch * 32 + lane;
-        const bool act = row < M.n_rows;
-        const int len = act ? __ldg(M.len + row) : 0;
+        const int srow = ch * 32 + lane;  // slot row (sorted order when perm != null)
+        const bool act = srow < M.n_rows;
+        const int len = act ? __ldg(M.len + srow) : 0;
+        const int row = act ? (M.perm ? __ldg(M.perm + srow) : srow) : 0;
         const int2 mw = __ldg(M.meta + ch);
         const long long base = (long long)mw.x * 32 + lane;
+        const double av = (act && need_aux) ? aux[row] : 0.0;
+        const double dw = (act && dotw) ? dotw[row] : 0.0;
         double s = 0.0;
-        for (int j0 = 0; j0 < mw.y; j0 += SELL_U) {
-            double v[SELL_U], xv[SELL_U];
-            int c[SELL_U];
+        for (int j0 = 0; j0 < mw.y; j0 += U) {
+            double v[U], xv[U];
+            int c[U];
 #pragma unroll
-            for (int u = 0; u < SELL_U; ++u) {
+            for (int u = 0; u < U; ++u) {
                 v[u] = 0.0;
                 c[u] = 0;
                 if (j0 + u < len) {
@@ -316,15 +349,22 @@ __global__ void __launch_bounds__(kBlock) k_sell(DSell M, int epi, const double*
                 }
             }
 #pragma unroll
-            for (int u = 0; u < SELL_U; ++u) xv[u] = (j0 + u < len) ? __ldg(x + c[u]) : 0.0;
+            for (int u = 0; u < U; ++u) xv[u] = (j0 + u < len) ? __ldg(x + c[u]) : 0.0;
 #pragma unroll
-            for (int u = 0; u < SELL_U; ++u)
+            for (int u = 0; u < U; ++u)
                 if (j0 + u < len) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
         }
         if (act) {
-            const double out = epilogue(epi, s, aux, row, omega);
+            double out;
+            switch (epi) {
+                case EPI_SCALE: out = __dmul_rn(omega, s); break;
+                case EPI_RESID: out = __dsub_rn(av, s); break;
+                case EPI_ADD: out = __dadd_rn(av, s); break;
+                case EPI_ADDSCALE: out = __dadd_rn(av, __dmul_rn(omega, s)); break;
+                default: out = s;
+            }
             y[row] = out;
-            if (dotw) dacc = fma(out, dotw[row], dacc);
+            if (dotw) dacc = fma(out, dw, dacc);
         }
     }
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
@@ -503,12 +543,14 @@ int spmv_grid(const DMat& M) {
         return M.sb.stream ? occ_grid(k_sbsr3<true>, (ch + 7) / 8) : occ_grid(k_sbsr3<false>, (ch + 7) / 8);
     }
     if (M.fmt == 2) {
-        const long long ch = M.sell.nchunks;
-        return M.sell.stream ? occ_grid(k_sell<true>, (ch + 7) / 8) : occ_grid(k_sell<false>, (ch + 7) / 8);
+        const long long ch = (M.sell.nchunks + 7) / 8;
+        if (M.sell.u <= 2) return occ_grid(k_sell<2, false>, ch);
+        if (M.sell.u <= 4) return occ_grid(k_sell<4, false>, ch);
+        return occ_grid(k_sell<8, false>, ch);
     }
-    const int G = M.csr.group;
-    const long long warps = ((long long)M.csr.n_rows * G + 31) / 32;
-    return occ_grid(k_csr<32, false>, (warps + 7) / 8);
+    const int T = M.csr.group;
+    const long long ctas = ((long long)M.csr.n_rows * T + kBlock - 1) / kBlock;
+    return occ_grid(k_csr<32, false>, ctas);
 }
 
 void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux, double omega, const double* dotw,
@@ -522,10 +564,19 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
         return;
     }
     if (M.fmt == 2) {
-        if (M.sell.stream)
-            k_sell<true><<<grid, kBlock, 0, L.stream>>>(M.sell, epi, x, y, aux, omega, dotw, red, done);
-        else
-            k_sell<false><<<grid, kBlock, 0, L.stream>>>(M.sell, epi, x, y, aux, omega, dotw, red, done);
+#define ASPAMG_SELL(UU)                                                                                      \
+    if (M.sell.stream)                                                                                       \
+        k_sell<UU, true><<<grid, kBlock, 0, L.stream>>>(M.sell, epi, x, y, aux, omega, dotw, red, done);    \
+    else                                                                                                     \
+        k_sell<UU, false><<<grid, kBlock, 0, L.stream>>>(M.sell, epi, x, y, aux, omega, dotw, red, done);
+        if (M.sell.u <= 2) {
+            ASPAMG_SELL(2)
+        } else if (M.sell.u <= 4) {
+            ASPAMG_SELL(4)
+        } else {
+            ASPAMG_SELL(8)
+        }
+#undef ASPAMG_SELL
         return;
     }
 #define ASPAMG_CSR_CASE(GG)                                                                                   \
@@ -541,8 +592,11 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
         ASPAMG_CSR_CASE(4)
         ASPAMG_CSR_CASE(8)
         ASPAMG_CSR_CASE(16)
-        default:
         ASPAMG_CSR_CASE(32)
+        ASPAMG_CSR_CASE(64)
+        ASPAMG_CSR_CASE(128)
+        default:
+        ASPAMG_CSR_CASE(256)
     }
 #undef ASPAMG_CSR_CASE
 }

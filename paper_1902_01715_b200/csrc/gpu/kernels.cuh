@@ -14,7 +14,7 @@ namespace aspamg_gpu {
 constexpr int kBlock = 256;  // threads per CTA for every streaming kernel
 
 // CSR, int32 offsets/columns. `group` = threads cooperating on one row
-// (power of two, 1..32), chosen from the mean row length at finalize.
+// (power of two, 1..256), chosen from the row lengths at upload.
 struct DCsr {
     int n_rows = 0, n_cols = 0;
     long long nnz = 0;
@@ -51,7 +51,9 @@ struct DSbsr3 {
 struct DSell {
     int n_rows = 0, n_cols = 0, nchunks = 0;
     long long nnz = 0, slots = 0;
-    int* len = nullptr;
+    int* perm = nullptr;  // SELL-32-sigma: slot row -> matrix row (null = natural order)
+    int* len = nullptr;   // per slot row
+    int u = 8;            // slots per load group (kernel variant)
     int2* meta = nullptr;
     int* ci = nullptr;
     double* v = nullptr;
