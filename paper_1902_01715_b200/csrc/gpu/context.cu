@@ -70,7 +70,7 @@ struct aspamg_gpu_ctx {
     // options
     int opt_bsr = 1, opt_device_loop = 1, opt_coarse_mode = 1;
     long long opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
-              opt_sell_u = 0;
+              opt_sell_u = 0, opt_sell_tma = 0;
     long long opt_stream_bytes = 48ll << 20;
     // PCG state and vectors
     PcgState* st = nullptr;       // device
@@ -316,6 +316,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         }
         S.stream = (long long)(12.0 * nnz) > c->opt_stream_bytes;
         S.u = c->opt_sell_u > 0 ? (int)c->opt_sell_u : (maxlen <= 4 ? 4 : 8);
+        S.tma = (int)c->opt_sell_tma;  // SEG*10 + stages, 0 = register pipeline
         return M;
     }
     M.fmt = 0;
@@ -687,6 +688,7 @@ int aspamg_gpu_ctx_create(int device, aspamg_gpu_ctx** out) {
         }
         if (device < 0 || device >= nd) throw Fail{4, "invalid device index"};
         CK(cudaSetDevice(device));
+        spmv_prepare();
         auto* c = new aspamg_gpu_ctx;
         c->device = device;
         cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -731,6 +733,8 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "sell_sigma") c->opt_sell_sigma = value;
         else if (k == "sell_sort_fill_pct") c->opt_sell_sort_fill_pct = value;
         else if (k == "sell_u") c->opt_sell_u = value;
+        else if (k == "sell_tma") c->opt_sell_tma = value;
+        else if (k == "pdl") set_pdl(value != 0);
         else if (k == "coarse_mode") c->opt_coarse_mode = (int)value;
         else throw Fail{4, "set_option: unknown key " + k};
     });

@@ -157,6 +157,15 @@ __device__ __forceinline__ bool is_done(const int* done) {
     return done != nullptr && *reinterpret_cast<const volatile int*>(done) != 0;
 }
 
+// Programmatic dependent launch (sm_90+): every kernel first waits for its
+// predecessor grid's completion + memory flush (no-op when launched without the
+// PDL attribute), then immediately allows its own successor to start launching,
+// so launch latency overlaps the previous kernel's tail instead of adding to it.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- CSR SpMV
 // T threads per row (power of two, 1..256); a CTA owns 256/T consecutive rows
 // per step (CTA-uniform loop, so barriers are legal). Each thread walks its
@@ -168,6 +177,7 @@ template <int T, bool STREAM>
 __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* __restrict__ x, double* y,
                                                  const double* aux, double omega, const double* dotw, Red red,
                                                  const int* done) {
+    pdl_enter();
     if (is_done(done)) return;
     constexpr int RPC = kBlock / T;  // rows per CTA step
     __shared__ double wsum[kBlock / 32];
@@ -236,6 +246,7 @@ template <bool STREAM>
 __global__ void __launch_bounds__(kBlock) k_sbsr3(DSbsr3 M, int epi, const double* __restrict__ x, double* y,
                                                    const double* aux, double omega, const double* dotw, Red red,
                                                    const int* done) {
+    pdl_enter();
     if (is_done(done)) return;
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -313,46 +324,255 @@ __global__ void __launch_bounds__(kBlock) k_sbsr3(DSbsr3 M, int epi, const doubl
 
 // ----------------------------------------------------------- SELL-32 SpMV
 // One lane per row; slot-major layout (coalesced); sequential ascending-column
-// sum with separate multiply/add (bit-identical to the reference spmv). The
-// epilogue operands (aux, dotw) are fetched with the first load group so the
-// chunk costs ~2 dependent memory round trips (values/columns, then x).
+// sum with separate multiply/add (bit-identical to the reference spmv).
+// Software pipeline: column indices are fetched one load group ahead (and the
+// next chunk's metadata + first column group during the current chunk), so
+// each group costs ONE memory round trip — values and x gathers are issued
+// together because the x addresses are already known.
+struct SellChunk {
+    int len, row, w;
+    long long base;
+    double av, dw;
+    bool act;
+};
+
+template <bool STREAM>
+__device__ __forceinline__ SellChunk sell_chunk(const DSell& M, int ch, int lane, bool need_aux, const double* aux,
+                                                const double* dotw) {
+    SellChunk c;
+    const int srow = ch * 32 + lane;
+    c.act = srow < M.n_rows;
+    c.len = c.act ? __ldg(M.len + srow) : 0;
+    c.row = c.act ? (M.perm ? __ldg(M.perm + srow) : srow) : 0;
+    const int2 mw = __ldg(M.meta + ch);
+    c.w = mw.y;
+    c.base = (long long)mw.x * 32 + lane;
+    c.av = (c.act && need_aux) ? aux[c.row] : 0.0;
+    c.dw = (c.act && dotw) ? dotw[c.row] : 0.0;
+    return c;
+}
+
 template <int U, bool STREAM>
 __global__ void __launch_bounds__(kBlock) k_sell(DSell M, int epi, const double* __restrict__ x, double* y,
                                                   const double* aux, double omega, const double* dotw, Red red,
                                                   const int* done) {
+    pdl_enter();
     if (is_done(done)) return;
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * kBlock) >> 5;
     const bool need_aux = epi == EPI_RESID || epi == EPI_ADD || epi == EPI_ADDSCALE;
     double dacc = 0.0;
+    int ch = warp;
+    SellChunk nx{};
+    int cn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cn[u] = 0;
+    if (ch < M.nchunks) {
+        nx = sell_chunk<STREAM>(M, ch, lane, need_aux, aux, dotw);
+#pragma unroll
+        for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? ld_mat<STREAM>(M.ci + nx.base + 32ll * u) : 0;
+    }
+    while (ch < M.nchunks) {
+        const SellChunk cu = nx;
+        const int chn = ch + nwarps;
+        if (chn < M.nchunks) nx = sell_chunk<STREAM>(M, chn, lane, need_aux, aux, dotw);
+        double s = 0.0;
+        for (int j0 = 0; j0 < cu.w; j0 += U) {
+            int cc[U];
+            double v[U], xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                cc[u] = cn[u];
+                const bool p = j0 + u < cu.len;
+                v[u] = p ? ld_mat<STREAM>(M.v + cu.base + 32ll * (j0 + u)) : 0.0;
+                xv[u] = p ? __ldg(x + cc[u]) : 0.0;
+            }
+            if (j0 + U < cu.w) {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    cn[u] = (j0 + U + u < cu.len) ? ld_mat<STREAM>(M.ci + cu.base + 32ll * (j0 + U + u)) : 0;
+            } else if (chn < M.nchunks) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? ld_mat<STREAM>(M.ci + nx.base + 32ll * u) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (j0 + u < cu.len) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+        }
+        if (cu.act) {
+            double out;
+            switch (epi) {
+                case EPI_SCALE: out = __dmul_rn(omega, s); break;
+                case EPI_RESID: out = __dsub_rn(cu.av, s); break;
+                case EPI_ADD: out = __dadd_rn(cu.av, s); break;
+                case EPI_ADDSCALE: out = __dadd_rn(cu.av, __dmul_rn(omega, s)); break;
+                default: out = s;
+            }
+            y[cu.row] = out;
+            if (dotw) dacc = fma(out, cu.dw, dacc);
+        }
+        ch = chn;
+    }
+    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
+}
+
+// ------------------------------------------------- SELL-32 SpMV, TMA-staged
+// Same SELL-32 layout and arithmetic as k_sell, but the matrix stream (values +
+// column indices of each chunk segment, two contiguous runs) is moved into a
+// per-warp shared-memory ring by cp.async.bulk (TMA bulk copies) completing on
+// mbarriers. Lane 0 keeps S segments in flight ahead of the consumer, so the
+// bytes in flight per SM are bounded by shared memory, not registers; the lanes
+// only issue the x gathers (addresses read from shared memory) and the sums.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+template <bool EVICT_FIRST>
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    if constexpr (EVICT_FIRST) {
+        unsigned long long pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                smem_u32(dst)),
+            "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+            : "memory");
+    } else {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(dst)),
+                     "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                     : "memory");
+    }
+}
+// Read-only gather whose issue order is pinned (volatile asm is not reordered
+// against other volatile asm): used to force a batch of independent gathers
+// to be in flight together before the dependent arithmetic.
+__device__ __forceinline__ double ldg_pinned(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int SEG, int S>
+struct SellTmaCfg {
+    static constexpr int kStageBytes = SEG * 384;                 // SEG slots x (32 doubles + 32 ints)
+    static constexpr int kWarpBytes = 128 + S * kStageBytes;       // barriers padded to 128 B
+    static constexpr int kBlockBytes = (kBlock / 32) * kWarpBytes;
+    static constexpr int kMinBlocks = (220 * 1024) / kBlockBytes < 1 ? 1 : ((220 * 1024) / kBlockBytes > 8 ? 8 : (220 * 1024) / kBlockBytes);
+};
+
+template <int SEG, int S, bool STREAM>
+__global__ void __launch_bounds__(kBlock, (SellTmaCfg<SEG, S>::kMinBlocks)) k_sell_tma(DSell M, int epi, const double* __restrict__ x, double* y,
+                                                      const double* aux, double omega, const double* dotw, Red red,
+                                                      const int* done) {
+    pdl_enter();
+    if (is_done(done)) return;
+    using Cfg = SellTmaCfg<SEG, S>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * kBlock) >> 5;
+    unsigned char* wbase = smem_raw + wib * Cfg::kWarpBytes;
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(wbase);
+    auto stage_v = [&](int st) { return reinterpret_cast<double*>(wbase + 128 + st * Cfg::kStageBytes); };
+    auto stage_c = [&](int st) { return reinterpret_cast<int*>(wbase + 128 + st * Cfg::kStageBytes + SEG * 256); };
+    if (lane == 0) {
+#pragma unroll
+        for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const bool need_aux = epi == EPI_RESID || epi == EPI_ADD || epi == EPI_ADDSCALE;
+
+    // producer cursor (uniform across the warp; lane 0 issues)
+    int pch = warp, pseg = 0, pw = 0, poff = 0;
+    if (pch < M.nchunks) {
+        const int2 m = __ldg(M.meta + pch);
+        poff = m.x;
+        pw = m.y;
+    }
+    auto issue = [&](int st) {
+        const int nsl = max(0, min(SEG, pw - pseg * SEG));
+        if (lane == 0) {
+            mbar_expect_tx(&bars[st], (unsigned)(nsl * 384));
+            if (nsl > 0) {
+                const long long slot = (long long)poff + (long long)pseg * SEG;
+                bulk_g2s<STREAM>(stage_v(st), M.v + slot * 32, (unsigned)(nsl * 256), &bars[st]);
+                bulk_g2s<STREAM>(stage_c(st), M.ci + slot * 32, (unsigned)(nsl * 128), &bars[st]);
+            }
+        }
+        ++pseg;
+        if (pseg * SEG >= max(pw, 1)) {
+            pch += nwarps;
+            pseg = 0;
+            if (pch < M.nchunks) {
+                const int2 m = __ldg(M.meta + pch);
+                poff = m.x;
+                pw = m.y;
+            }
+        }
+    };
+#pragma unroll
+    for (int st = 0; st < S; ++st)
+        if (pch < M.nchunks) issue(st);
+
+    double dacc = 0.0;
+    unsigned parity = 0;  // bit st = phase of stage st
+    int stage = 0;
     for (int ch = warp; ch < M.nchunks; ch += nwarps) {
-        const int srow = ch * 32 + lane;  // slot row (sorted order when perm != null)
+        const int srow = ch * 32 + lane;
         const bool act = srow < M.n_rows;
         const int len = act ? __ldg(M.len + srow) : 0;
         const int row = act ? (M.perm ? __ldg(M.perm + srow) : srow) : 0;
-        const int2 mw = __ldg(M.meta + ch);
-        const long long base = (long long)mw.x * 32 + lane;
         const double av = (act && need_aux) ? aux[row] : 0.0;
         const double dw = (act && dotw) ? dotw[row] : 0.0;
+        const int w = __ldg(M.meta + ch).y;
+        const int nseg = max(1, (w + SEG - 1) / SEG);
         double s = 0.0;
-        for (int j0 = 0; j0 < mw.y; j0 += U) {
-            double v[U], xv[U];
-            int c[U];
+        for (int sg = 0; sg < nseg; ++sg) {
+            mbar_wait(&bars[stage], (parity >> stage) & 1u);
+            parity ^= 1u << stage;
+            const double* sv = stage_v(stage);
+            const int* sc = stage_c(stage);
+            const int j0 = sg * SEG;
+            // all SEG gathers issued before the first use (padding reads x[0], never used)
+            int ci[SEG];
+            double xv[SEG];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                v[u] = 0.0;
-                c[u] = 0;
-                if (j0 + u < len) {
-                    v[u] = ld_mat<STREAM>(M.v + base + 32ll * (j0 + u));
-                    c[u] = ld_mat<STREAM>(M.ci + base + 32ll * (j0 + u));
-                }
+            for (int j = 0; j < SEG; ++j) ci[j] = (j0 + j < len) ? sc[j * 32 + lane] : 0;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) xv[j] = ldg_pinned(x + ci[j]);
+#pragma unroll
+            for (int j = 0; j < SEG; ++j)
+                if (j0 + j < len) s = __dadd_rn(s, __dmul_rn(sv[j * 32 + lane], xv[j]));
+            __syncwarp();
+            if (pch < M.nchunks) {
+                if (lane == 0) fence_proxy_async();
+                issue(stage);
             }
-#pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = (j0 + u < len) ? __ldg(x + c[u]) : 0.0;
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (j0 + u < len) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+            stage = stage + 1 == S ? 0 : stage + 1;
         }
         if (act) {
             double out;
@@ -376,6 +596,7 @@ __global__ void __launch_bounds__(kBlock) k_sell(DSell M, int epi, const double*
 __global__ void __launch_bounds__(kBlock) k_trmv(int n, int upper, const double* __restrict__ W,
                                                   const double* __restrict__ x, double* y, const double* dotw,
                                                   Red red, const int* done) {
+    pdl_enter();
     if (is_done(done)) return;
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -399,6 +620,7 @@ __global__ void __launch_bounds__(kBlock) k_trmv(int n, int upper, const double*
 // ------------------------------------------------------------- PCG vectors
 __global__ void __launch_bounds__(kBlock) k_pcg_p(int n, const double* __restrict__ z, double* __restrict__ p,
                                                    const PcgState* st, const int* done) {
+    pdl_enter();
     if (is_done(done)) return;
     const bool first = st->k == 0;
     const double beta = st->beta;
@@ -409,6 +631,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_p(int n, const double* __restric
 __global__ void __launch_bounds__(kBlock) k_pcg_xr(int n, double* __restrict__ x, double* __restrict__ r,
                                                     const double* __restrict__ p, const double* __restrict__ q,
                                                     Red red, const int* done) {
+    pdl_enter();
     if (is_done(done)) {
         if (red.use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(red.cond, 0u);
         return;
@@ -426,6 +649,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_xr(int n, double* __restrict__ x
 
 __global__ void __launch_bounds__(kBlock) k_pcg_init(int n, const double* __restrict__ b, const double* __restrict__ r,
                                                       Red red) {
+    pdl_enter();
     double s = 0.0, s2 = 0.0;
     for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
         s = fma(b[i], b[i], s);
@@ -435,6 +659,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_init(int n, const double* __rest
 }
 
 __global__ void __launch_bounds__(kBlock) k_zero(int n, double* y, const int* done) {
+    pdl_enter();
     if (is_done(done)) return;
     for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) y[i] = 0.0;
 }
@@ -453,6 +678,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse(int n, const double* 
                                                             const double* __restrict__ Dinv_b,
                                                             const double* __restrict__ y, double* z,
                                                             const double* dotw, Red red, const int* done) {
+    pdl_enter();
     if (is_done(done)) return;
     extern __shared__ double zs[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -511,6 +737,25 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse(int n, const double* 
     if (red.fin != FIN_NONE) reduce_finish(acc, red);
 }
 
+bool g_pdl = true;
+
+// Launch through cudaLaunchKernelEx so the PDL attribute can be attached; the
+// attribute is recorded into CUDA graphs as a programmatic dependency edge.
+template <class... KArgs, class... Args>
+void launch(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 int g_num_sms = 0;
 int num_sms() {
     if (g_num_sms == 0) {
@@ -523,11 +768,9 @@ int num_sms() {
 }
 
 template <class K>
-int occ_grid(K kern, long long work_units_per_cta_needed) {
-    static int cache[64];
-    (void)cache;
+int occ_grid(K kern, long long work_units_per_cta_needed, size_t smem = 0) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
     if (per_sm <= 0) per_sm = 1;
     long long g = (long long)num_sms() * per_sm;
     if (work_units_per_cta_needed < g) g = work_units_per_cta_needed;
@@ -539,18 +782,49 @@ int occ_grid(K kern, long long work_units_per_cta_needed) {
 // ------------------------------------------------------------------ host API
 int spmv_grid(const DMat& M) {
     if (M.fmt == 1) {
-        const long long ch = M.sb.nchunks;
-        return M.sb.stream ? occ_grid(k_sbsr3<true>, (ch + 7) / 8) : occ_grid(k_sbsr3<false>, (ch + 7) / 8);
+        const long long ch = (M.sb.nchunks + 7) / 8;
+        return M.sb.stream ? occ_grid(k_sbsr3<true>, ch) : occ_grid(k_sbsr3<false>, ch);
+    }
+    if (M.fmt == 2 && M.sell.tma) {
+        const long long ch = (M.sell.nchunks + 7) / 8;
+        const bool st = M.sell.stream;
+#define ASPAMG_TMA_OCC(SG, SS)                                                                  \
+    if (M.sell.tma == SG * 10 + SS)                                                             \
+        return st ? occ_grid(k_sell_tma<SG, SS, true>, ch, SellTmaCfg<SG, SS>::kBlockBytes)     \
+                  : occ_grid(k_sell_tma<SG, SS, false>, ch, SellTmaCfg<SG, SS>::kBlockBytes);
+        ASPAMG_TMA_OCC(16, 4)
+        ASPAMG_TMA_OCC(16, 2)
+        ASPAMG_TMA_OCC(8, 4)
+        ASPAMG_TMA_OCC(8, 2)
+        ASPAMG_TMA_OCC(4, 4)
+#undef ASPAMG_TMA_OCC
+        return 1;
     }
     if (M.fmt == 2) {
         const long long ch = (M.sell.nchunks + 7) / 8;
-        if (M.sell.u <= 2) return occ_grid(k_sell<2, false>, ch);
-        if (M.sell.u <= 4) return occ_grid(k_sell<4, false>, ch);
-        return occ_grid(k_sell<8, false>, ch);
+        const bool st = M.sell.stream;
+        if (M.sell.u <= 2) return st ? occ_grid(k_sell<2, true>, ch) : occ_grid(k_sell<2, false>, ch);
+        if (M.sell.u <= 4) return st ? occ_grid(k_sell<4, true>, ch) : occ_grid(k_sell<4, false>, ch);
+        return st ? occ_grid(k_sell<8, true>, ch) : occ_grid(k_sell<8, false>, ch);
     }
     const int T = M.csr.group;
     const long long ctas = ((long long)M.csr.n_rows * T + kBlock - 1) / kBlock;
-    return occ_grid(k_csr<32, false>, ctas);
+    const bool st = M.csr.stream;
+#define ASPAMG_CSR_OCC(TT) \
+    case TT: return st ? occ_grid(k_csr<TT, true>, ctas) : occ_grid(k_csr<TT, false>, ctas);
+    switch (T) {
+        ASPAMG_CSR_OCC(1)
+        ASPAMG_CSR_OCC(2)
+        ASPAMG_CSR_OCC(4)
+        ASPAMG_CSR_OCC(8)
+        ASPAMG_CSR_OCC(16)
+        ASPAMG_CSR_OCC(32)
+        ASPAMG_CSR_OCC(64)
+        ASPAMG_CSR_OCC(128)
+        default:
+        ASPAMG_CSR_OCC(256)
+    }
+#undef ASPAMG_CSR_OCC
 }
 
 void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux, double omega, const double* dotw,
@@ -558,17 +832,36 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
     const int grid = L.grid > 0 ? L.grid : spmv_grid(M);
     if (M.fmt == 1) {
         if (M.sb.stream)
-            k_sbsr3<true><<<grid, kBlock, 0, L.stream>>>(M.sb, epi, x, y, aux, omega, dotw, red, done);
+            launch(k_sbsr3<true>, grid, kBlock, 0, L.stream, M.sb, epi, x, y, aux, omega, dotw, red, done);
         else
-            k_sbsr3<false><<<grid, kBlock, 0, L.stream>>>(M.sb, epi, x, y, aux, omega, dotw, red, done);
+            launch(k_sbsr3<false>, grid, kBlock, 0, L.stream, M.sb, epi, x, y, aux, omega, dotw, red, done);
+        return;
+    }
+    if (M.fmt == 2 && M.sell.tma) {
+#define ASPAMG_SELLT(SG, SS)                                                                                  \
+    if (M.sell.tma == SG * 10 + SS) {                                                                         \
+        if (M.sell.stream)                                                                                    \
+            launch(k_sell_tma<SG, SS, true>, grid, kBlock, SellTmaCfg<SG, SS>::kBlockBytes, L.stream,        \
+                   M.sell, epi, x, y, aux, omega, dotw, red, done);                                              \
+        else                                                                                                  \
+            launch(k_sell_tma<SG, SS, false>, grid, kBlock, SellTmaCfg<SG, SS>::kBlockBytes, L.stream,       \
+                   M.sell, epi, x, y, aux, omega, dotw, red, done);                                              \
+        return;                                                                                               \
+    }
+        ASPAMG_SELLT(16, 4)
+        ASPAMG_SELLT(16, 2)
+        ASPAMG_SELLT(8, 4)
+        ASPAMG_SELLT(8, 2)
+        ASPAMG_SELLT(4, 4)
+#undef ASPAMG_SELLT
         return;
     }
     if (M.fmt == 2) {
 #define ASPAMG_SELL(UU)                                                                                      \
     if (M.sell.stream)                                                                                       \
-        k_sell<UU, true><<<grid, kBlock, 0, L.stream>>>(M.sell, epi, x, y, aux, omega, dotw, red, done);    \
+        launch(k_sell<UU, true>, grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);    \
     else                                                                                                     \
-        k_sell<UU, false><<<grid, kBlock, 0, L.stream>>>(M.sell, epi, x, y, aux, omega, dotw, red, done);
+        launch(k_sell<UU, false>, grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);
         if (M.sell.u <= 2) {
             ASPAMG_SELL(2)
         } else if (M.sell.u <= 4) {
@@ -582,9 +875,9 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
 #define ASPAMG_CSR_CASE(GG)                                                                                   \
     case GG:                                                                                                  \
         if (M.csr.stream)                                                                                     \
-            k_csr<GG, true><<<grid, kBlock, 0, L.stream>>>(M.csr, epi, x, y, aux, omega, dotw, red, done);   \
+            launch(k_csr<GG, true>, grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);   \
         else                                                                                                  \
-            k_csr<GG, false><<<grid, kBlock, 0, L.stream>>>(M.csr, epi, x, y, aux, omega, dotw, red, done);  \
+            launch(k_csr<GG, false>, grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);  \
         break;
     switch (M.csr.group) {
         ASPAMG_CSR_CASE(1)
@@ -607,30 +900,49 @@ int vec_grid(int n) {
 }
 
 void pcg_p(int n, const double* z, double* p, const PcgState* st, const int* done, const Launch& L) {
-    k_pcg_p<<<L.grid > 0 ? L.grid : vec_grid(n), kBlock, 0, L.stream>>>(n, z, p, st, done);
+    launch(k_pcg_p, L.grid > 0 ? L.grid : vec_grid(n), kBlock, 0, L.stream, n, z, p, st, done);
 }
 
 void pcg_xr(int n, double* x, double* r, const double* p, const double* q, const Red& red, const int* done,
             const Launch& L) {
-    k_pcg_xr<<<L.grid > 0 ? L.grid : vec_grid(n), kBlock, 0, L.stream>>>(n, x, r, p, q, red, done);
+    launch(k_pcg_xr, L.grid > 0 ? L.grid : vec_grid(n), kBlock, 0, L.stream, n, x, r, p, q, red, done);
 }
 
 void pcg_init_dots(int n, const double* b, const double* r, const Red& red, const Launch& L) {
-    k_pcg_init<<<L.grid > 0 ? L.grid : vec_grid(n), kBlock, 0, L.stream>>>(n, b, r, red);
+    launch(k_pcg_init, L.grid > 0 ? L.grid : vec_grid(n), kBlock, 0, L.stream, n, b, r, red);
 }
 
 void coarse_solve(int n, const double* Lrm, const double* Lcm, const double* Dinv_f, const double* Dinv_b,
                   const double* y, double* z, const double* dotw, const Red& red, const int* done,
                   const Launch& L) {
     const size_t smem = sizeof(double) * (size_t)(n > 0 ? n : 1);
-    k_coarse<<<1, kCoarseThreads, smem, L.stream>>>(n, Lrm, Lcm, Dinv_f, Dinv_b, y, z, dotw, red, done);
+    launch(k_coarse, 1, kCoarseThreads, smem, L.stream, n, Lrm, Lcm, Dinv_f, Dinv_b, y, z, dotw, red, done);
 }
 
 int trmv_grid(int n) { return occ_grid(k_trmv, ((long long)n + 7) / 8); }
 
 void trmv(int n, bool upper, const double* W, const double* x, double* y, const double* dotw, const Red& red,
           const int* done, const Launch& L) {
-    k_trmv<<<L.grid > 0 ? L.grid : trmv_grid(n), kBlock, 0, L.stream>>>(n, upper ? 1 : 0, W, x, y, dotw, red, done);
+    launch(k_trmv, L.grid > 0 ? L.grid : trmv_grid(n), kBlock, 0, L.stream, n, upper ? 1 : 0, W, x, y, dotw, red, done);
+}
+
+void set_pdl(bool on) { g_pdl = on; }
+
+void spmv_prepare() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+#define ASPAMG_TMA_ATTR(SG, SS)                                                                                      \
+    cudaFuncSetAttribute(k_sell_tma<SG, SS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                      \
+                         SellTmaCfg<SG, SS>::kBlockBytes);                                                           \
+    cudaFuncSetAttribute(k_sell_tma<SG, SS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
+                         SellTmaCfg<SG, SS>::kBlockBytes);
+    ASPAMG_TMA_ATTR(16, 4)
+    ASPAMG_TMA_ATTR(16, 2)
+    ASPAMG_TMA_ATTR(8, 4)
+    ASPAMG_TMA_ATTR(8, 2)
+    ASPAMG_TMA_ATTR(4, 4)
+#undef ASPAMG_TMA_ATTR
 }
 
 void coarse_prepare(int n) {
@@ -639,7 +951,7 @@ void coarse_prepare(int n) {
 }
 
 void fill_zero(int n, double* y, const int* done, const Launch& L) {
-    k_zero<<<L.grid > 0 ? L.grid : vec_grid(n), kBlock, 0, L.stream>>>(n, y, done);
+    launch(k_zero, L.grid > 0 ? L.grid : vec_grid(n), kBlock, 0, L.stream, n, y, done);
 }
 
 }  // namespace aspamg_gpu

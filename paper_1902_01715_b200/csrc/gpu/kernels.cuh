@@ -53,7 +53,8 @@ struct DSell {
     long long nnz = 0, slots = 0;
     int* perm = nullptr;  // SELL-32-sigma: slot row -> matrix row (null = natural order)
     int* len = nullptr;   // per slot row
-    int u = 8;            // slots per load group (kernel variant)
+    int u = 8;            // slots per load group (register-pipelined variant)
+    int tma = 0;          // 0: register pipeline; SEG*10+S: TMA-staged ring (164, 162, 84, 82, 44)
     int2* meta = nullptr;
     int* ci = nullptr;
     double* v = nullptr;
@@ -143,6 +144,8 @@ void trmv(int n, bool upper, const double* Wrm, const double* x, double* y, cons
           const int* done, const Launch& L);
 int trmv_grid(int n);
 
+void set_pdl(bool on);          // programmatic dependent launch on/off (process-wide)
+void spmv_prepare();          // once per process, outside any stream capture
 void coarse_prepare(int n);  // once per factor size, outside any stream capture
 void fill_zero(int n, double* y, const int* done, const Launch& L);
 
