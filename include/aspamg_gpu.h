@@ -99,6 +99,9 @@ int aspamg_gpu_pcg_device(aspamg_gpu_ctx* ctx, const double* b_dev, const double
 int aspamg_gpu_last_solve_ms(aspamg_gpu_ctx* ctx, double* ms);      /* device time of the last pcg */
 int aspamg_gpu_launch_count(aspamg_gpu_ctx* ctx, int64_t* n);       /* kernels launched by the last pcg */
 int aspamg_gpu_profile_iteration(aspamg_gpu_ctx* ctx, aspamg_gpu_kernel_time* out, int cap, int* count);
+int aspamg_gpu_time_vcycle(aspamg_gpu_ctx* ctx, int reps, double* avg_ms); /* standalone V-cycle graph */
+/* graph-mode per-op time: each op of the PCG body replayed `reps` times inside one CUDA graph */
+int aspamg_gpu_profile_ops(aspamg_gpu_ctx* ctx, int reps, aspamg_gpu_kernel_time* out, int cap, int* count);
 int aspamg_gpu_time_kernel(aspamg_gpu_ctx* ctx, const char* name, int64_t level, int reps,
                            double* avg_ms, double* alg_bytes);
 int aspamg_gpu_stream(aspamg_gpu_ctx* ctx, void** stream);

@@ -136,6 +136,8 @@ def gpu() -> C.CDLL:
         lib.aspamg_gpu_level_info.argtypes = [vp, i64, C.POINTER(GpuLevelInfo)]
         lib.aspamg_gpu_num_levels.argtypes = [vp, P_i64]
         lib.aspamg_gpu_profile_iteration.argtypes = [vp, C.POINTER(GpuKernelTime), C.c_int, C.POINTER(C.c_int)]
+        lib.aspamg_gpu_profile_ops.argtypes = [vp, C.c_int, C.POINTER(GpuKernelTime), C.c_int, C.POINTER(C.c_int)]
+        lib.aspamg_gpu_time_vcycle.argtypes = [vp, C.c_int, P_dbl]
         lib.aspamg_gpu_time_kernel.argtypes = [vp, C.c_char_p, i64, C.c_int, P_dbl, P_dbl]
         lib.aspamg_gpu_launch_count.argtypes = [vp, P_i64]
         lib.aspamg_gpu_last_solve_ms.argtypes = [vp, P_dbl]

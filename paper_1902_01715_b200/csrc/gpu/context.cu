@@ -64,14 +64,15 @@ struct aspamg_gpu_ctx {
     // coarsest factor
     int n_c = 0;
     double *Lrm = nullptr, *Lcm = nullptr, *Dinv_f = nullptr, *Dinv_b = nullptr;
-    double *Wrm = nullptr, *Wt = nullptr, *cw = nullptr;  // W = L^{-1} (lower), W' (upper), temp
+    double* cw = nullptr;  // temp between the two triangular products
+    DMat Wm, Wtm;          // W = L^{-1} (lower) and W' (upper) as CSR operands
     bool coarse_uploaded = false;
     bool finalized = false;
     // options
     int opt_bsr = 1, opt_device_loop = 1, opt_coarse_mode = 1;
-    long long opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
+    long long opt_sell_min_rows = 65536, opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
               opt_sell_u = 0, opt_sell_tma = 0;
-    long long opt_stream_bytes = 48ll << 20;
+    long long opt_stream_bytes = 48ll << 20, opt_keep_bytes = 64ll << 20;
     // PCG state and vectors
     PcgState* st = nullptr;       // device
     PcgState* st_host = nullptr;  // pinned
@@ -195,10 +196,20 @@ void check_view(const aspamg_csr_view* v, const char* what) {
 
 // Threads per row for the CSR kernel: ~4+ entries per thread, widened for
 // small levels so the grid still covers the GPU (>= ~150k threads).
-int group_for(double mean, int64_t n_rows) {
+// Threads per row for the CSR kernel: ~4+ entries per thread for the mean
+// row, at most ~16 sequential entries for the longest row (its serial chain
+// sets the kernel latency on small levels), and widened for small levels so
+// the grid still covers the GPU (>= ~150k threads).
+// Threads per row for the CSR kernel: ~8 entries per thread for the mean row;
+// on small operands (< 64k rows, where the longest row's serial chain sets the
+// kernel latency) also <= ~32 sequential entries for the longest row, and
+// widened so the grid still covers the GPU (>= ~150k threads).
+int group_for(double mean, int maxlen, int64_t n_rows) {
     int g = 1;
     while (g < 256 && 4.0 * 2 * g <= mean) g *= 2;
-    while (g < 256 && (double)n_rows * g < 150000.0 && 2.0 * g <= mean) g *= 2;
+    if (n_rows < 65536)
+        while (g < 256 && 32 * g < maxlen) g *= 2;
+    while (g < 256 && (double)n_rows * g < 150000.0 && 2.0 * g <= std::max(mean, 1.0)) g *= 2;
     return g;
 }
 
@@ -256,7 +267,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         CK(cudaMemcpy(B.meta, meta.data(), meta.size() * sizeof(int2), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(B.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(B.v, val.data(), val.size() * sizeof(double), cudaMemcpyHostToDevice));
-        B.stream = (long long)(76.0 * B.nnzb) > c->opt_stream_bytes;
+        B.pol = (long long)(76.0 * B.nnzb) > c->opt_stream_bytes ? 1 : 0;
         return M;
     }
     std::vector<int> len((size_t)std::max<int64_t>(v.n_rows, 0), 0);
@@ -265,7 +276,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         len[(size_t)i] = (int)(v.row_offsets[i + 1] - v.row_offsets[i]);
         maxlen = std::max(maxlen, len[(size_t)i]);
     }
-    if (v.n_rows > 0 && mean <= (double)c->opt_sell_max_mean && maxlen <= c->opt_sell_max_len) {
+    if (v.n_rows >= c->opt_sell_min_rows && mean <= (double)c->opt_sell_max_mean && maxlen <= c->opt_sell_max_len) {
         M.fmt = 2;
         DSell& S = M.sell;
         S.n_rows = (int)v.n_rows;
@@ -314,8 +325,8 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
             S.perm = dalloc<int>(c, perm.size());
             CK(cudaMemcpy(S.perm, perm.data(), perm.size() * sizeof(int), cudaMemcpyHostToDevice));
         }
-        S.stream = (long long)(12.0 * nnz) > c->opt_stream_bytes;
-        S.u = c->opt_sell_u > 0 ? (int)c->opt_sell_u : (maxlen <= 4 ? 4 : 8);
+        S.pol = (long long)(12.0 * nnz) > c->opt_stream_bytes ? 1 : 0;
+        S.u = c->opt_sell_u > 0 ? (int)c->opt_sell_u : (maxlen <= 4 ? 41 : 83);  // U*10 + min CTAs/SM
         S.tma = (int)c->opt_sell_tma;  // SEG*10 + stages, 0 = register pipeline
         return M;
     }
@@ -335,9 +346,21 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         CK(cudaMemcpy(A.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(A.v, v.values, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice));
     }
-    A.group = group_for(mean, v.n_rows);
-    A.stream = (long long)(12.0 * nnz) > c->opt_stream_bytes;
+    A.group = group_for(mean, maxlen, v.n_rows);
+    A.pol = (long long)(12.0 * nnz) > c->opt_stream_bytes ? 1 : 0;
     return M;
+}
+
+// Device bytes of an operand's matrix stream (what one product reads).
+double mat_bytes(const DMat& M) {
+    if (M.fmt == 1) return 76.0 * 32.0 * double(M.sb.slots) + 4.0 * M.sb.nb;
+    if (M.fmt == 2) return 12.0 * 32.0 * double(M.sell.slots) + 4.0 * M.sell.n_rows;
+    return 12.0 * double(M.csr.nnz) + 4.0 * (M.csr.n_rows + 1);
+}
+void set_pol(DMat& M, int pol) {
+    if (M.fmt == 1) M.sb.pol = pol;
+    else if (M.fmt == 2) M.sell.pol = pol;
+    else M.csr.pol = pol;
 }
 
 // Stored (padded) entries / true nnz of an operand.
@@ -389,17 +412,9 @@ void build_vcycle(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* 
         const int n = c->n_c;
         const double* dw = top ? dotw0 : nullptr;
         if (c->opt_coarse_mode == 1) {
-            if (top && fin0 != FIN_NONE) red = make_red(c, trmv_grid(n), fin0);
-            const double *W = c->Wrm, *Wt = c->Wt;
-            double* w = c->cw;
-            const int g = trmv_grid(n);
-            const double bytes = 8.0 * double(n) * (n + 1) / 2 + 16.0 * n;
-            ops.push_back({"coarse_fwd", k, bytes, [=](cudaStream_t s) {
-                               trmv(n, false, W, y, w, nullptr, Red{}, done, Launch{g, s});
-                           }});
-            ops.push_back({"coarse_bwd", k, bytes + (dw ? 8.0 * n : 0.0), [=](cudaStream_t s) {
-                               trmv(n, true, Wt, w, z, dw, red, done, Launch{g, s});
-                           }});
+            add_spmv(c, ops, "coarse_fwd", k, c->Wm, EPI_PLAIN, y, c->cw, nullptr, 1.0, nullptr, FIN_NONE, nullptr, done);
+            add_spmv(c, ops, "coarse_bwd", k, c->Wtm, EPI_PLAIN, c->cw, z, nullptr, 1.0, dw, top ? fin0 : FIN_NONE,
+                     nullptr, done);
             return;
         }
         if (top && fin0 != FIN_NONE) red = make_red(c, 1, fin0);
@@ -542,6 +557,25 @@ void do_finalize(aspamg_gpu_ctx* c) {
         if (k + 1 < L) {
             l.r = dalloc<double>(c, l.n);
             l.t = dalloc<double>(c, l.n);
+        }
+    }
+    // L2 policy: the coarsest levels (bottom-up, up to keep_bytes) are loaded
+    // with evict-last so they stay L2-resident across V-cycles; everything
+    // bigger than stream_bytes streams with evict-first.
+    {
+        double kept = mat_bytes(c->Wm) + mat_bytes(c->Wtm);
+        set_pol(c->Wm, 2);
+        set_pol(c->Wtm, 2);
+        for (int k = L - 1; k >= 0; --k) {
+            GLevel& l = c->lv[(size_t)k];
+            DMat* ms[5] = {&l.A, &l.G, &l.Gt, &l.P, &l.Pt};
+            double b = 0.0;
+            for (int i = 0; i < 5; ++i)
+                if (i == 0 || l.has_smoother) b += mat_bytes(*ms[i]);
+            if (kept + b > (double)c->opt_keep_bytes) break;
+            kept += b;
+            for (int i = 0; i < 5; ++i)
+                if (i == 0 || l.has_smoother) set_pol(*ms[i], 2);
         }
     }
     const int* done = &c->st->done;
@@ -728,8 +762,10 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         if (k == "bsr") c->opt_bsr = (int)value;
         else if (k == "device_loop") c->opt_device_loop = (int)value;
         else if (k == "stream_bytes") c->opt_stream_bytes = value;
+        else if (k == "keep_bytes") c->opt_keep_bytes = value;
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;
         else if (k == "sell_max_len") c->opt_sell_max_len = value;
+        else if (k == "sell_min_rows") c->opt_sell_min_rows = value;
         else if (k == "sell_sigma") c->opt_sell_sigma = value;
         else if (k == "sell_sort_fill_pct") c->opt_sell_sort_fill_pct = value;
         else if (k == "sell_u") c->opt_sell_u = value;
@@ -839,11 +875,27 @@ int aspamg_gpu_upload_coarse(aspamg_gpu_ctx* c, int64_t n_c, const double* Lc) {
         for (int i = 0; i < n; ++i)
             for (int j = 0; j <= i; ++j) Wt[(size_t)j * n + i] = W[(size_t)i * n + j];
         c->n_c = n;
-        c->Wrm = dalloc<double>(c, W.size());
-        c->Wt = dalloc<double>(c, Wt.size());
         c->cw = dalloc<double>(c, (size_t)n);
-        CK(cudaMemcpy(c->Wrm, W.data(), W.size() * 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->Wt, Wt.data(), Wt.size() * 8, cudaMemcpyHostToDevice));
+        {  // dense triangles as CSR (row-contiguous, ascending columns)
+            std::vector<int64_t> rpl((size_t)n + 1), rpu((size_t)n + 1), cil, ciu;
+            std::vector<double> vl, vu;
+            cil.reserve((size_t)n * (n + 1) / 2);
+            ciu.reserve((size_t)n * (n + 1) / 2);
+            vl.reserve(cil.capacity());
+            vu.reserve(ciu.capacity());
+            for (int i = 0; i < n; ++i) {
+                rpl[(size_t)i] = (int64_t)cil.size();
+                for (int j = 0; j <= i; ++j) { cil.push_back(j); vl.push_back(W[(size_t)i * n + j]); }
+                rpu[(size_t)i] = (int64_t)ciu.size();
+                for (int j = i; j < n; ++j) { ciu.push_back(j); vu.push_back(Wt[(size_t)i * n + j]); }
+            }
+            rpl[(size_t)n] = (int64_t)cil.size();
+            rpu[(size_t)n] = (int64_t)ciu.size();
+            aspamg_csr_view lv{n, n, (int64_t)cil.size(), rpl.data(), cil.data(), vl.data()};
+            aspamg_csr_view uv{n, n, (int64_t)ciu.size(), rpu.data(), ciu.data(), vu.data()};
+            c->Wm = upload_mat(c, lv, false);
+            c->Wtm = upload_mat(c, uv, false);
+        }
         c->Lrm = dalloc<double>(c, rm.size());
         c->Lcm = dalloc<double>(c, cm.size());
         c->Dinv_f = dalloc<double>(c, df.size());
@@ -987,8 +1039,8 @@ int aspamg_gpu_coarse_solve(aspamg_gpu_ctx* c, const double* y, double* z) {
         CK(cudaMalloc(&dz, bytes));
         cudaMemcpyAsync(dy, y, bytes, cudaMemcpyHostToDevice, c->stream);
         if (c->opt_coarse_mode == 1) {
-            trmv(c->n_c, false, c->Wrm, dy, c->cw, nullptr, Red{}, nullptr, Launch{0, c->stream});
-            trmv(c->n_c, true, c->Wt, c->cw, dz, nullptr, Red{}, nullptr, Launch{0, c->stream});
+            spmv(c->Wm, EPI_PLAIN, dy, c->cw, nullptr, 1.0, nullptr, Red{}, nullptr, Launch{0, c->stream});
+            spmv(c->Wtm, EPI_PLAIN, c->cw, dz, nullptr, 1.0, nullptr, Red{}, nullptr, Launch{0, c->stream});
         } else {
             coarse_solve(c->n_c, c->Lrm, c->Lcm, c->Dinv_f, c->Dinv_b, dy, dz, nullptr, Red{}, nullptr,
                          Launch{1, c->stream});
@@ -1113,6 +1165,73 @@ int aspamg_gpu_profile_iteration(aspamg_gpu_ctx* c, aspamg_gpu_kernel_time* out,
         }
         *count = k;
         for (auto& e : ev) cudaEventDestroy(e);
+        CK(cudaGetLastError());
+    });
+}
+
+// Device time of the standalone V-cycle graph (y = vy -> z = vz), averaged.
+int aspamg_gpu_time_vcycle(aspamg_gpu_ctx* c, int reps, double* avg_ms) {
+    return guard(c, [&] {
+        ensure_ready(c);
+        CK(cudaSetDevice(c->device));
+        reps = std::max(1, reps);
+        for (int i = 0; i < 3; ++i) CK(cudaGraphLaunch(c->vc_exec, c->stream));
+        CK(cudaEventRecord(c->ev0, c->stream));
+        for (int i = 0; i < reps; ++i) CK(cudaGraphLaunch(c->vc_exec, c->stream));
+        CK(cudaEventRecord(c->ev1, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        *avg_ms = ms / reps;
+    });
+}
+
+// Graph-mode per-op timing: each body op is captured `reps` times back to back
+// into its own graph; the per-launch time includes the in-graph launch gap.
+int aspamg_gpu_profile_ops(aspamg_gpu_ctx* c, int reps, aspamg_gpu_kernel_time* out, int cap, int* count) {
+    return guard(c, [&] {
+        ensure_ready(c);
+        CK(cudaSetDevice(c->device));
+        cudaStream_t s = c->stream;
+        reps = std::max(1, std::min(reps, 64));
+        CK(cudaMemcpyAsync(c->st_host, c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        PcgState h = *c->st_host;
+        h.done = 0; h.notspd = 0; h.k = 1; h.tol = 0.0; h.max_it = 1ll << 40;
+        if (!c->hist || c->hist_cap < 4096) {
+            if (c->hist) cudaFree(c->hist);
+            c->hist_cap = 4096;
+            CK(cudaMalloc(&c->hist, (size_t)c->hist_cap * sizeof(double)));
+        }
+        h.history = c->hist;
+        if (!(h.bnorm > 0)) h.bnorm = 1.0;
+        if (!(h.rz != 0)) h.rz = 1.0;
+        int k = 0;
+        for (size_t i = 0; i < c->body.size() && k < cap; ++i, ++k) {
+            std::vector<Op> rep(reps, c->body[i]);
+            cudaGraph_t g = capture(c, rep);
+            cudaGraphExec_t ge = nullptr;
+            CK(cudaGraphInstantiate(&ge, g, 0));
+            h.k = 1;
+            *c->st_host = h;
+            CK(cudaMemcpyAsync(c->st, c->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+            CK(cudaGraphLaunch(ge, s));  // warm
+            CK(cudaMemcpyAsync(c->st, c->st_host, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+            CK(cudaEventRecord(c->ev0, s));
+            CK(cudaGraphLaunch(ge, s));
+            CK(cudaEventRecord(c->ev1, s));
+            CK(cudaStreamSynchronize(s));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+            cudaGraphExecDestroy(ge);
+            cudaGraphDestroy(g);
+            std::memset(&out[k], 0, sizeof(out[k]));
+            std::strncpy(out[k].name, c->body[i].name.c_str(), sizeof(out[k].name) - 1);
+            out[k].level = c->body[i].level;
+            out[k].ms = ms / reps;
+            out[k].alg_bytes = c->body[i].bytes;
+        }
+        *count = k;
         CK(cudaGetLastError());
     });
 }

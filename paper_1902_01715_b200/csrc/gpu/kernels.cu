@@ -147,9 +147,28 @@ __device__ __forceinline__ double epilogue(int epi, double s, const double* aux,
     }
 }
 
-template <bool STREAM, class T>
+// Matrix-stream load with an L2 policy: POL 0 default, 1 evict-first
+// (operators much larger than L2 stream through it), 2 evict-last (the small
+// coarse levels stay L2-resident across V-cycles).
+__device__ __forceinline__ unsigned long long l2_keep_policy() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double ld_keep(const double* p) {
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(l2_keep_policy()));
+    return r;
+}
+__device__ __forceinline__ int ld_keep(const int* p) {
+    int r;
+    asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(l2_keep_policy()));
+    return r;
+}
+template <int POL, class T>
 __device__ __forceinline__ T ld_mat(const T* p) {
-    if constexpr (STREAM) return __ldcs(p);
+    if constexpr (POL == 1) return __ldcs(p);
+    else if constexpr (POL == 2) return ld_keep(p);
     else return __ldg(p);
 }
 
@@ -173,7 +192,7 @@ __device__ __forceinline__ void pdl_enter() {
 // a fixed shuffle tree (and, for T > 32, a fixed smem combine of the warp sums).
 constexpr int CSR_U = 4;
 
-template <int T, bool STREAM>
+template <int T, int STREAM>
 __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* __restrict__ x, double* y,
                                                  const double* aux, double omega, const double* dotw, Red red,
                                                  const int* done) {
@@ -242,7 +261,7 @@ constexpr int SB_U = 3;    // block slots per load group (sliced BSR3)
 // row sums run sequentially in ascending column order with separate multiply
 // and add — exactly the reference spmv's arithmetic (sparse_matrix.cpp:100-105),
 // so y is bit-identical to it.
-template <bool STREAM>
+template <int STREAM>
 __global__ void __launch_bounds__(kBlock) k_sbsr3(DSbsr3 M, int epi, const double* __restrict__ x, double* y,
                                                    const double* aux, double omega, const double* dotw, Red red,
                                                    const int* done) {
@@ -336,7 +355,7 @@ struct SellChunk {
     bool act;
 };
 
-template <bool STREAM>
+template <int STREAM>
 __device__ __forceinline__ SellChunk sell_chunk(const DSell& M, int ch, int lane, bool need_aux, const double* aux,
                                                 const double* dotw) {
     SellChunk c;
@@ -352,8 +371,8 @@ __device__ __forceinline__ SellChunk sell_chunk(const DSell& M, int ch, int lane
     return c;
 }
 
-template <int U, bool STREAM>
-__global__ void __launch_bounds__(kBlock) k_sell(DSell M, int epi, const double* __restrict__ x, double* y,
+template <int U, int STREAM, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const double* __restrict__ x, double* y,
                                                   const double* aux, double omega, const double* dotw, Red red,
                                                   const int* done) {
     pdl_enter();
@@ -590,33 +609,6 @@ __global__ void __launch_bounds__(kBlock, (SellTmaCfg<SEG, S>::kMinBlocks)) k_se
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
 }
 
-// ------------------------------------------------ dense triangular mat-vec
-// y = W x for W lower (row i: j <= i) or upper (row i: j >= i) stored dense
-// row-major; one warp per row, lane-strided coalesced loads, fixed tree sum.
-__global__ void __launch_bounds__(kBlock) k_trmv(int n, int upper, const double* __restrict__ W,
-                                                  const double* __restrict__ x, double* y, const double* dotw,
-                                                  Red red, const int* done) {
-    pdl_enter();
-    if (is_done(done)) return;
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * kBlock) >> 5;
-    double dacc = 0.0;
-    for (int i = warp; i < n; i += nwarps) {
-        const double* row = W + (long long)i * n;
-        const int j0 = upper ? i : 0, j1 = upper ? n : i + 1;
-        double s = 0.0;
-#pragma unroll 4
-        for (int j = j0 + lane; j < j1; j += 32) s = fma(__ldg(row + j), __ldg(x + j), s);
-        s = warp_sum(s);
-        if (lane == 0) {
-            y[i] = s;
-            if (dotw) dacc = fma(s, dotw[i], dacc);
-        }
-    }
-    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
-}
-
 // ------------------------------------------------------------- PCG vectors
 __global__ void __launch_bounds__(kBlock) k_pcg_p(int n, const double* __restrict__ z, double* __restrict__ p,
                                                    const PcgState* st, const int* done) {
@@ -783,11 +775,11 @@ int occ_grid(K kern, long long work_units_per_cta_needed, size_t smem = 0) {
 int spmv_grid(const DMat& M) {
     if (M.fmt == 1) {
         const long long ch = (M.sb.nchunks + 7) / 8;
-        return M.sb.stream ? occ_grid(k_sbsr3<true>, ch) : occ_grid(k_sbsr3<false>, ch);
+        return M.sb.pol == 1 ? occ_grid(k_sbsr3<1>, ch) : M.sb.pol == 2 ? occ_grid(k_sbsr3<2>, ch) : occ_grid(k_sbsr3<0>, ch);
     }
     if (M.fmt == 2 && M.sell.tma) {
         const long long ch = (M.sell.nchunks + 7) / 8;
-        const bool st = M.sell.stream;
+        const bool st = M.sell.pol == 1;
 #define ASPAMG_TMA_OCC(SG, SS)                                                                  \
     if (M.sell.tma == SG * 10 + SS)                                                             \
         return st ? occ_grid(k_sell_tma<SG, SS, true>, ch, SellTmaCfg<SG, SS>::kBlockBytes)     \
@@ -802,16 +794,26 @@ int spmv_grid(const DMat& M) {
     }
     if (M.fmt == 2) {
         const long long ch = (M.sell.nchunks + 7) / 8;
-        const bool st = M.sell.stream;
-        if (M.sell.u <= 2) return st ? occ_grid(k_sell<2, true>, ch) : occ_grid(k_sell<2, false>, ch);
-        if (M.sell.u <= 4) return st ? occ_grid(k_sell<4, true>, ch) : occ_grid(k_sell<4, false>, ch);
-        return st ? occ_grid(k_sell<8, true>, ch) : occ_grid(k_sell<8, false>, ch);
+        const int st = M.sell.pol;
+#define ASPAMG_SELL_OCC(UU, MB)                                                                  \
+    if (M.sell.u == UU * 10 + MB)                                                                \
+        return st == 1 ? occ_grid(k_sell<UU, 1, MB>, ch)                                         \
+                       : st == 2 ? occ_grid(k_sell<UU, 2, MB>, ch) : occ_grid(k_sell<UU, 0, MB>, ch);
+        ASPAMG_SELL_OCC(8, 1)
+        ASPAMG_SELL_OCC(8, 3)
+        ASPAMG_SELL_OCC(8, 4)
+        ASPAMG_SELL_OCC(4, 1)
+        ASPAMG_SELL_OCC(4, 4)
+        ASPAMG_SELL_OCC(4, 6)
+        ASPAMG_SELL_OCC(2, 1)
+#undef ASPAMG_SELL_OCC
+        return 1;
     }
     const int T = M.csr.group;
     const long long ctas = ((long long)M.csr.n_rows * T + kBlock - 1) / kBlock;
-    const bool st = M.csr.stream;
+    const int st = M.csr.pol;
 #define ASPAMG_CSR_OCC(TT) \
-    case TT: return st ? occ_grid(k_csr<TT, true>, ctas) : occ_grid(k_csr<TT, false>, ctas);
+    case TT: return st == 1 ? occ_grid(k_csr<TT, 1>, ctas) : st == 2 ? occ_grid(k_csr<TT, 2>, ctas) : occ_grid(k_csr<TT, 0>, ctas);
     switch (T) {
         ASPAMG_CSR_OCC(1)
         ASPAMG_CSR_OCC(2)
@@ -831,16 +833,18 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
           const Red& red, const int* done, const Launch& L) {
     const int grid = L.grid > 0 ? L.grid : spmv_grid(M);
     if (M.fmt == 1) {
-        if (M.sb.stream)
-            launch(k_sbsr3<true>, grid, kBlock, 0, L.stream, M.sb, epi, x, y, aux, omega, dotw, red, done);
+        if (M.sb.pol == 1)
+            launch(k_sbsr3<1>, grid, kBlock, 0, L.stream, M.sb, epi, x, y, aux, omega, dotw, red, done);
+        else if (M.sb.pol == 2)
+            launch(k_sbsr3<2>, grid, kBlock, 0, L.stream, M.sb, epi, x, y, aux, omega, dotw, red, done);
         else
-            launch(k_sbsr3<false>, grid, kBlock, 0, L.stream, M.sb, epi, x, y, aux, omega, dotw, red, done);
+            launch(k_sbsr3<0>, grid, kBlock, 0, L.stream, M.sb, epi, x, y, aux, omega, dotw, red, done);
         return;
     }
     if (M.fmt == 2 && M.sell.tma) {
 #define ASPAMG_SELLT(SG, SS)                                                                                  \
     if (M.sell.tma == SG * 10 + SS) {                                                                         \
-        if (M.sell.stream)                                                                                    \
+        if (M.sell.pol == 1)                                                                                  \
             launch(k_sell_tma<SG, SS, true>, grid, kBlock, SellTmaCfg<SG, SS>::kBlockBytes, L.stream,        \
                    M.sell, epi, x, y, aux, omega, dotw, red, done);                                              \
         else                                                                                                  \
@@ -857,27 +861,34 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
         return;
     }
     if (M.fmt == 2) {
-#define ASPAMG_SELL(UU)                                                                                      \
-    if (M.sell.stream)                                                                                       \
-        launch(k_sell<UU, true>, grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);    \
-    else                                                                                                     \
-        launch(k_sell<UU, false>, grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);
-        if (M.sell.u <= 2) {
-            ASPAMG_SELL(2)
-        } else if (M.sell.u <= 4) {
-            ASPAMG_SELL(4)
-        } else {
-            ASPAMG_SELL(8)
-        }
+#define ASPAMG_SELL(UU, MB)                                                                                          \
+    if (M.sell.u == UU * 10 + MB) {                                                                                 \
+        if (M.sell.pol == 1)                                                                                        \
+            launch(k_sell<UU, 1, MB>, grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);     \
+        else if (M.sell.pol == 2)                                                                                   \
+            launch(k_sell<UU, 2, MB>, grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);     \
+        else                                                                                                        \
+            launch(k_sell<UU, 0, MB>, grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);     \
+        return;                                                                                                     \
+    }
+        ASPAMG_SELL(8, 1)
+        ASPAMG_SELL(8, 3)
+        ASPAMG_SELL(8, 4)
+        ASPAMG_SELL(4, 1)
+        ASPAMG_SELL(4, 4)
+        ASPAMG_SELL(4, 6)
+        ASPAMG_SELL(2, 1)
 #undef ASPAMG_SELL
         return;
     }
 #define ASPAMG_CSR_CASE(GG)                                                                                   \
     case GG:                                                                                                  \
-        if (M.csr.stream)                                                                                     \
-            launch(k_csr<GG, true>, grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);   \
+        if (M.csr.pol == 1)                                                                                   \
+            launch(k_csr<GG, 1>, grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
+        else if (M.csr.pol == 2)                                                                              \
+            launch(k_csr<GG, 2>, grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
         else                                                                                                  \
-            launch(k_csr<GG, false>, grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);  \
+            launch(k_csr<GG, 0>, grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
         break;
     switch (M.csr.group) {
         ASPAMG_CSR_CASE(1)
@@ -917,13 +928,6 @@ void coarse_solve(int n, const double* Lrm, const double* Lcm, const double* Din
                   const Launch& L) {
     const size_t smem = sizeof(double) * (size_t)(n > 0 ? n : 1);
     launch(k_coarse, 1, kCoarseThreads, smem, L.stream, n, Lrm, Lcm, Dinv_f, Dinv_b, y, z, dotw, red, done);
-}
-
-int trmv_grid(int n) { return occ_grid(k_trmv, ((long long)n + 7) / 8); }
-
-void trmv(int n, bool upper, const double* W, const double* x, double* y, const double* dotw, const Red& red,
-          const int* done, const Launch& L) {
-    launch(k_trmv, L.grid > 0 ? L.grid : trmv_grid(n), kBlock, 0, L.stream, n, upper ? 1 : 0, W, x, y, dotw, red, done);
 }
 
 void set_pdl(bool on) { g_pdl = on; }

@@ -22,7 +22,7 @@ struct DCsr {
     int* ci = nullptr;
     double* v = nullptr;
     int group = 1;
-    bool stream = false;  // evict-first loads (matrix larger than ~L2/2)
+    int pol = 0;  // L2 policy of the matrix stream: 0 default, 1 evict-first, 2 evict-last
 };
 
 // Sliced 3x3-block format for an exactly 3x3-blocked operator (K): block
@@ -41,7 +41,7 @@ struct DSbsr3 {
     int2* meta = nullptr;           // per chunk {off, width}
     int* ci = nullptr;
     double* v = nullptr;
-    bool stream = false;
+    int pol = 0;
 };
 
 // SELL-32 (sliced ELL, chunk height 32, no sorting): one lane per row,
@@ -53,12 +53,12 @@ struct DSell {
     long long nnz = 0, slots = 0;
     int* perm = nullptr;  // SELL-32-sigma: slot row -> matrix row (null = natural order)
     int* len = nullptr;   // per slot row
-    int u = 8;            // slots per load group (register-pipelined variant)
+    int u = 81;           // register-pipelined variant: U*10 + min CTAs/SM (81, 83, 84, 41, 44, 46, 21)
     int tma = 0;          // 0: register pipeline; SEG*10+S: TMA-staged ring (164, 162, 84, 82, 44)
     int2* meta = nullptr;
     int* ci = nullptr;
     double* v = nullptr;
-    bool stream = false;
+    int pol = 0;
 };
 
 // One matrix operand.
@@ -136,13 +136,9 @@ int vec_grid(int n);
 //         Dinv_f / Dinv_b inverted 32x32 diagonal blocks).
 // mode 1: the two triangular solves applied through the explicit inverse
 //         factor W = L^{-1} (computed once at upload): w = W y, z = W' w, each a
-//         multi-CTA warp-per-row triangular mat-vec (Wrm: row-major W, lower;
-//         Wt: row-major W', upper).
+//         multi-CTA CSR product over the dense triangle (context.cu).
 void coarse_solve(int n, const double* Lrm, const double* Lcm, const double* Dinv_f, const double* Dinv_b,
                   const double* y, double* z, const double* dotw, const Red& red, const int* done, const Launch& L);
-void trmv(int n, bool upper, const double* Wrm, const double* x, double* y, const double* dotw, const Red& red,
-          const int* done, const Launch& L);
-int trmv_grid(int n);
 
 void set_pdl(bool on);          // programmatic dependent launch on/off (process-wide)
 void spmv_prepare();          // once per process, outside any stream capture

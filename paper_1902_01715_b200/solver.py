@@ -374,6 +374,20 @@ class GpuVcycle:
         return [(buf[i].name.decode(), int(buf[i].level), float(buf[i].ms), float(buf[i].alg_bytes))
                 for i in range(cnt.value)]
 
+    def profile_ops(self, reps: int = 20) -> list[tuple[str, int, float, float]]:
+        """Graph-mode per-op times (each op replayed ``reps`` times in one graph)."""
+        buf = (N.GpuKernelTime * 512)()
+        cnt = C.c_int()
+        self._chk(self._lib.aspamg_gpu_profile_ops(self._ctx, reps, buf, 512, C.byref(cnt)))
+        return [(buf[i].name.decode(), int(buf[i].level), float(buf[i].ms), float(buf[i].alg_bytes))
+                for i in range(cnt.value)]
+
+    def time_vcycle(self, reps: int = 50) -> float:
+        """Average device ms of one V-cycle (its CUDA graph, launched back to back)."""
+        ms = C.c_double()
+        self._chk(self._lib.aspamg_gpu_time_vcycle(self._ctx, reps, C.byref(ms)))
+        return ms.value
+
     def time_kernel(self, name: str, level: int, reps: int = 20) -> tuple[float, float]:
         ms = C.c_double()
         by = C.c_double()

@@ -54,12 +54,13 @@ def main():
         for _ in range(3):
             x, rep = g.pcg(prob.rhs)
             t.append(rep.T_s / max(rep.iterations, 1))
-        prof = g.profile_iteration()
-        res[name] = {"opts": opts, "s_per_it": min(t), "n_it": rep.iterations,
-                     "eager_ms": sum(p[2] for p in prof),
+        vms = g.time_vcycle(50)
+        prof = g.profile_ops(reps=20)
+        res[name] = {"opts": opts, "s_per_it": min(t), "n_it": rep.iterations, "vcycle_ms": vms,
+                     "graph_ops_ms": sum(p[2] for p in prof),
                      "kernels": [(p[0], p[1], round(p[2] * 1e3, 1), round(p[3] / (p[2] * 1e-3) / 1e9) if p[2] else 0)
                                  for p in prof]}
-        print(f"{name:10s} {min(t)*1e3:.4f} ms/it  eager {res[name]['eager_ms']:.3f} ms  n_it {rep.iterations}",
+        print(f"{name:10s} {min(t)*1e3:.4f} ms/it  vcycle {vms:.4f} ms  ops {res[name]['graph_ops_ms']:.3f} ms  n_it {rep.iterations}",
               flush=True)
         g.close()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
