@@ -34,6 +34,8 @@ struct Op {
     int level;
     double bytes;  // algorithmic bytes (compulsory traffic)
     std::function<void(cudaStream_t)> fn;
+    bool describable = false;  // expressible as a TailOp (CSR product / zero fill, no reduction)
+    TailOp desc{};
 };
 
 struct GLevel {
@@ -72,7 +74,7 @@ struct aspamg_gpu_ctx {
     int opt_bsr = 1, opt_device_loop = 1, opt_coarse_mode = 1;
     long long opt_sell_min_rows = 65536, opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
               opt_sell_u = 0, opt_sell_tma = 0;
-    long long opt_stream_bytes = 48ll << 20, opt_keep_bytes = 64ll << 20;
+    long long opt_stream_bytes = 48ll << 20, opt_keep_bytes = 64ll << 20, opt_tail_rows = 0;
     // PCG state and vectors
     PcgState* st = nullptr;       // device
     PcgState* st_host = nullptr;  // pinned
@@ -399,14 +401,52 @@ void add_spmv(aspamg_gpu_ctx* c, std::vector<Op>& ops, const std::string& name, 
                        Launch L{grid, s};
                        spmv(Mc, epi, x, y, aux, omega, dotw, red, done, L);
                    }});
+    if (M.fmt == 0 && fin == FIN_NONE && !dotw) {
+        Op& o = ops.back();
+        o.describable = true;
+        o.desc.kind = 0;
+        o.desc.epi = epi;
+        o.desc.M = M.csr;
+        o.desc.x = x;
+        o.desc.y = y;
+        o.desc.aux = aux;
+        o.desc.omega = omega;
+        o.desc.n = M.rows();
+    }
 }
 
 // V-cycle ops at level k: input y, output z (z doubles as the s accumulator).
 // dotw0/fin0: the dot fused into the last op that writes the level-0 output.
 void build_vcycle(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* y, double* z, const double* dotw0,
-                  int fin0, const int* done) {
+                  int fin0, const int* done, bool allow_tail = true);
+
+// Levels k.. (all smaller than tail_rows) as one persistent cooperative kernel.
+bool build_tail(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* y, double* z, const int* done) {
+    std::vector<Op> sub;
+    build_vcycle(c, sub, k, y, z, nullptr, FIN_NONE, done, false);
+    for (const Op& o : sub)
+        if (!o.describable) return false;
+    std::vector<TailOp> d;
+    double bytes = 0.0;
+    for (const Op& o : sub) {
+        d.push_back(o.desc);
+        bytes += o.bytes;
+    }
+    TailOp* dd = dalloc<TailOp>(c, d.size());
+    CK(cudaMemcpy(dd, d.data(), d.size() * sizeof(TailOp), cudaMemcpyHostToDevice));
+    GridBar* bar = dalloc<GridBar>(c, 1);
+    CK(cudaMemset(bar, 0, sizeof(GridBar)));
+    const int grid = tail_grid();
+    const int nops = (int)d.size();
+    ops.push_back({"tail" + std::to_string(nops), k, bytes, [=](cudaStream_t s) { tail_run(dd, nops, bar, done, grid, s); }});
+    return true;
+}
+
+void build_vcycle(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* y, double* z, const double* dotw0,
+                  int fin0, const int* done, bool allow_tail) {
     const int L = (int)c->lv.size();
     const bool top = k == 0;
+    if (allow_tail && k >= 1 && c->lv[(size_t)k].n <= c->opt_tail_rows && build_tail(c, ops, k, y, z, done)) return;
     if (k == L - 1) {  // coarsest: forward/backward solve
         Red red;
         const int n = c->n_c;
@@ -446,11 +486,15 @@ void build_vcycle(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* 
     if (c->nu1 == 0) {
         const int g = vec_grid(n);
         ops.push_back({"zero", k, 8.0 * n, [=](cudaStream_t st) { fill_zero(n, s, done, Launch{g, st}); }});
+        ops.back().describable = true;
+        ops.back().desc.kind = 1;
+        ops.back().desc.y = s;
+        ops.back().desc.n = n;
     }
     // r = y - A s ; r_c = P' r
     add_spmv(c, ops, "resid_A", k, l.A, EPI_RESID, s, l.r, y, 1.0, nullptr, FIN_NONE, nullptr, done);
     add_spmv(c, ops, "restrict_Pt", k, l.Pt, EPI_PLAIN, l.r, yc, nullptr, 1.0, nullptr, FIN_NONE, nullptr, done);
-    build_vcycle(c, ops, k + 1, yc, zc, dotw0, fin0, done);
+    build_vcycle(c, ops, k + 1, yc, zc, dotw0, fin0, done, allow_tail);
     // s += P e_c
     const bool last_is_prolong = c->nu2 == 0;
     add_spmv(c, ops, "prolong_P", k, l.P, EPI_ADD, zc, s, s, 1.0, (top && last_is_prolong) ? dotw0 : nullptr,
@@ -763,6 +807,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "device_loop") c->opt_device_loop = (int)value;
         else if (k == "stream_bytes") c->opt_stream_bytes = value;
         else if (k == "keep_bytes") c->opt_keep_bytes = value;
+        else if (k == "tail_rows") c->opt_tail_rows = value;
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;
         else if (k == "sell_max_len") c->opt_sell_max_len = value;
         else if (k == "sell_min_rows") c->opt_sell_min_rows = value;

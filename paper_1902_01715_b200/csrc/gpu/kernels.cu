@@ -609,6 +609,106 @@ __global__ void __launch_bounds__(kBlock, (SellTmaCfg<SEG, S>::kMinBlocks)) k_se
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
 }
 
+// ------------------------------------------------------------- coarse tail
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Sense-reversing software grid barrier (all CTAs co-resident: cooperative
+// launch sized to the occupancy). Thread 0's gpu-scope fences order the CTA's
+// writes before the arrival and invalidate L1 after the release.
+__device__ __forceinline__ void grid_barrier(GridBar* b) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = ld_acquire_u32(&b->gen);
+        __threadfence();
+        if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
+            atomicExch(&b->count, 0u);
+            __threadfence();
+            atomicAdd(&b->gen, 1u);
+        } else {
+            while (ld_acquire_u32(&b->gen) == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// One CSR product op inside the persistent kernel: runtime T (power of two,
+// 1..256) threads per row, same per-thread order and trees as k_csr. Vector
+// operands written earlier in the same kernel are read through L2 (__ldcg).
+__device__ void tail_csr(const TailOp& op, double* wsum) {
+    const DCsr& M = op.M;
+    const int T = M.group;
+    const int RPC = kBlock / T;
+    const int t = threadIdx.x & (T - 1);
+    const int lr = threadIdx.x / T;
+    const int lane = threadIdx.x & 31;
+    for (int rbase = blockIdx.x * RPC; rbase < M.n_rows; rbase += gridDim.x * RPC) {
+        const int row = rbase + lr;
+        double s = 0.0;
+        if (row < M.n_rows) {
+            const int b = __ldg(M.rp + row), e = __ldg(M.rp + row + 1);
+            for (int k0 = b + t; k0 < e; k0 += T * CSR_U) {
+                double v[CSR_U], xv[CSR_U];
+                int c[CSR_U];
+#pragma unroll
+                for (int u = 0; u < CSR_U; ++u) {
+                    const int kk = k0 + u * T;
+                    v[u] = kk < e ? __ldg(M.v + kk) : 0.0;
+                    c[u] = kk < e ? __ldg(M.ci + kk) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < CSR_U; ++u) xv[u] = (k0 + u * T < e) ? __ldcg(op.x + c[u]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < CSR_U; ++u) s = fma(v[u], xv[u], s);
+            }
+        }
+        if (T <= 32) {
+            for (int o = T / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, T);
+        } else {
+            s = warp_sum(s);
+            if (lane == 0) wsum[threadIdx.x >> 5] = s;
+            __syncthreads();
+            if (t == 0) {
+                double a = 0.0;
+                for (int w = 0; w < T / 32; ++w) a += wsum[(threadIdx.x >> 5) + w];
+                s = a;
+            }
+            __syncthreads();
+        }
+        if (t == 0 && row < M.n_rows) {
+            double out;
+            switch (op.epi) {
+                case EPI_SCALE: out = __dmul_rn(op.omega, s); break;
+                case EPI_RESID: out = __dsub_rn(__ldcg(op.aux + row), s); break;
+                case EPI_ADD: out = __dadd_rn(__ldcg(op.aux + row), s); break;
+                case EPI_ADDSCALE: out = __dadd_rn(__ldcg(op.aux + row), __dmul_rn(op.omega, s)); break;
+                default: out = s;
+            }
+            op.y[row] = out;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_tail(const TailOp* __restrict__ ops, int nops, GridBar* bar,
+                                                  const int* done) {
+    pdl_enter();
+    if (is_done(done)) return;
+    __shared__ double wsum[kBlock / 32];
+    for (int i = 0; i < nops; ++i) {
+        const TailOp op = ops[i];
+        if (op.kind == 0) {
+            tail_csr(op, wsum);
+        } else {
+            for (int r = blockIdx.x * kBlock + threadIdx.x; r < op.n; r += gridDim.x * kBlock) op.y[r] = 0.0;
+        }
+        if (i + 1 < nops) grid_barrier(bar);
+    }
+}
+
 // ------------------------------------------------------------- PCG vectors
 __global__ void __launch_bounds__(kBlock) k_pcg_p(int n, const double* __restrict__ z, double* __restrict__ p,
                                                    const PcgState* st, const int* done) {
@@ -931,6 +1031,28 @@ void coarse_solve(int n, const double* Lrm, const double* Lcm, const double* Din
 }
 
 void set_pdl(bool on) { g_pdl = on; }
+
+int tail_grid() {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail, kBlock, 0);
+    if (per_sm <= 0) per_sm = 1;
+    return num_sms() * per_sm;
+}
+
+void tail_run(const TailOp* ops, int nops, GridBar* bar, const int* done, int grid, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)kBlock);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the software grid barrier
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, k_tail, ops, nops, bar, done);
+}
 
 void spmv_prepare() {
     static bool done = false;

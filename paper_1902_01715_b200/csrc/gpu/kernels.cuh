@@ -140,6 +140,28 @@ int vec_grid(int n);
 void coarse_solve(int n, const double* Lrm, const double* Lcm, const double* Dinv_f, const double* Dinv_b,
                   const double* y, double* z, const double* dotw, const Red& red, const int* done, const Launch& L);
 
+// ------------------------------------------------------------ coarse tail
+// The small levels of the V-cycle run as ONE persistent kernel that walks a
+// device-side op table (CSR products with epilogues, zero fills) with a
+// software grid barrier between ops: the ~20 launches / drains of the tail
+// become one launch; all CTAs are co-resident (cooperative launch).
+struct TailOp {
+    int kind;  // 0 CSR product, 1 zero fill
+    int epi;
+    DCsr M;
+    const double* x;
+    double* y;
+    const double* aux;
+    double omega;
+    int n;     // rows for kind 1
+};
+struct GridBar {
+    unsigned count;
+    unsigned gen;
+};
+void tail_run(const TailOp* ops, int nops, GridBar* bar, const int* done, int grid, cudaStream_t s);
+int tail_grid();
+
 void set_pdl(bool on);          // programmatic dependent launch on/off (process-wide)
 void spmv_prepare();          // once per process, outside any stream capture
 void coarse_prepare(int n);  // once per factor size, outside any stream capture

@@ -257,3 +257,16 @@ def test_one_level_hierarchy_is_direct_solve(pkg, oracle):
     assert rel_err(K @ z, y) < 1e-10
     x, rep = g.pcg(p.rhs)
     assert rep.iterations == 1 and rep.converged  # exact preconditioner
+
+
+@pytest.mark.parametrize("tail_rows", [10000, 2000])
+def test_coarse_tail_persistent_kernel_matches_oracle(pkg, oracle, tail_rows):
+    """Levels below tail_rows run as one persistent cooperative kernel; same results."""
+    p, h = problem_and_hierarchy(1, 1)
+    g = _gpu(pkg, h, tail_rows=tail_rows)
+    o = _oracle(oracle, h)
+    y = np.random.default_rng(21).standard_normal(p.K.n_rows)
+    assert rel_err(g.apply(y), o.vcycle(y)) < RTOL_VCYCLE
+    ref = _gpu(pkg, h)
+    assert np.array_equal(g.apply(y), ref.apply(y))  # same kernels' arithmetic, same bits
+    _pcg_parity(p, h, g, o)
