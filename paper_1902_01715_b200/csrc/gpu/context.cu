@@ -73,7 +73,7 @@ struct aspamg_gpu_ctx {
     // options
     int opt_bsr = 1, opt_device_loop = 1, opt_coarse_mode = 1;
     long long opt_sell_min_rows = 65536, opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
-              opt_sell_u = 0, opt_sell_tma = 0;
+              opt_sell_u = 0, opt_sell_tma = 0, opt_sell_chh = 0;
     long long opt_stream_bytes = 48ll << 20, opt_keep_bytes = 64ll << 20, opt_tail_rows = 0;
     // PCG state and vectors
     PcgState* st = nullptr;       // device
@@ -217,14 +217,17 @@ int group_for(double mean, int maxlen, int64_t n_rows) {
 
 // Chunk metadata of a sliced layout: rows (or block rows) in chunks of 32,
 // chunk width = longest row of the chunk.
-void slice_meta(const std::vector<int>& len, std::vector<int2>& meta, long long& slots) {
+// Chunk metadata of a sliced layout: rows (or block rows) in chunks of h,
+// chunk width = longest row of the chunk; `slots` counts padded slot rows of
+// h entries (entry (j, r) of chunk q lives at (off_q + j) * h + r).
+void slice_meta(const std::vector<int>& len, std::vector<int2>& meta, long long& slots, int h = 32) {
     const int n = (int)len.size();
-    const int nch = (n + 31) / 32;
+    const int nch = (n + h - 1) / h;
     meta.resize((size_t)std::max(nch, 1));
     slots = 0;
     for (int ch = 0; ch < nch; ++ch) {
         int w = 0;
-        for (int l = 0; l < 32 && ch * 32 + l < n; ++l) w = std::max(w, len[(size_t)ch * 32 + l]);
+        for (int l = 0; l < h && ch * h + l < n; ++l) w = std::max(w, len[(size_t)ch * h + l]);
         if (slots > (1ll << 31) / 288) throw Fail{4, "sliced layout exceeds int32 slot indexing"};
         meta[(size_t)ch] = make_int2((int)slots, w);
         slots += w;
@@ -285,13 +288,25 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         S.n_cols = (int)v.n_cols;
         S.nnz = nnz;
         S.nchunks = (S.n_rows + 31) / 32;
+        // Layout choice by padded bytes, natural order preferred (x-gather locality):
+        // SELL-32 natural -> SELL-8 natural -> SELL-32-sigma (rows sorted by
+        // length, descending, inside windows of sigma rows).
         std::vector<int2> meta;
-        slice_meta(len, meta, S.slots);
-        // SELL-32-sigma: rows sorted by length (descending, stable) inside windows of
-        // sigma rows when the natural order pads too much.
+        long long s32 = 0, s8 = 0;
+        slice_meta(len, meta, s32, 32);
+        std::vector<int2> meta8;
+        slice_meta(len, meta8, s8, 8);
+        const double f32 = nnz ? double(s32) * 32.0 / double(nnz) : 1.0;
+        const double f8 = nnz ? double(s8) * 8.0 / double(nnz) : 1.0;
+        const double lim = (double)c->opt_sell_sort_fill_pct / 100.0;
         std::vector<int> perm;
         std::vector<int> slen = len;
-        if (nnz > 0 && double(S.slots) * 32.0 / double(nnz) > (double)c->opt_sell_sort_fill_pct / 100.0) {
+        int h = 32;
+        if (c->opt_sell_chh == 8 || (c->opt_sell_chh == 0 && !c->opt_sell_tma && f32 > lim && f8 <= lim)) {
+            h = 8;
+            meta.swap(meta8);
+            S.slots = s8;
+        } else if (c->opt_sell_chh == 0 && f32 > lim && nnz > 0) {
             const int64_t sigma = std::max<int64_t>(32, c->opt_sell_sigma);
             perm.resize((size_t)v.n_rows);
             for (int64_t i = 0; i < v.n_rows; ++i) perm[(size_t)i] = (int)i;
@@ -301,20 +316,25 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
                                  [&](int a, int b) { return len[(size_t)a] > len[(size_t)b]; });
             }
             for (int64_t i = 0; i < v.n_rows; ++i) slen[(size_t)i] = len[(size_t)perm[(size_t)i]];
-            slice_meta(slen, meta, S.slots);
+            slice_meta(slen, meta, S.slots, 32);
+        } else {
+            S.slots = s32;
         }
-        std::vector<int> ci((size_t)std::max<long long>(S.slots * 32, 1), 0);
+        S.chh = h;
+        // S.slots counts slot rows of h entries; store padded entries / 32 for the byte accounting
+        std::vector<int> ci((size_t)std::max<long long>(S.slots * h, 1), 0);
         std::vector<double> val(ci.size(), 0.0);
         for (int64_t sr = 0; sr < v.n_rows; ++sr) {
             const int64_t i = perm.empty() ? sr : perm[(size_t)sr];
-            const long long off = meta[(size_t)(sr / 32)].x;
-            const int lane = (int)(sr % 32);
+            const long long off = meta[(size_t)(sr / h)].x;
+            const int r = (int)(sr % h);
             for (int64_t k = v.row_offsets[i]; k < v.row_offsets[i + 1]; ++k) {
                 const long long j = k - v.row_offsets[i];
-                ci[(size_t)((off + j) * 32 + lane)] = (int)v.col_indices[k];
-                val[(size_t)((off + j) * 32 + lane)] = v.values[k];
+                ci[(size_t)((off + j) * h + r)] = (int)v.col_indices[k];
+                val[(size_t)((off + j) * h + r)] = v.values[k];
             }
         }
+        S.slots = (S.slots * h + 31) / 32;  // padded entries / 32 (byte accounting, as for SELL-32)
         S.len = dalloc<int>(c, slen.size());
         S.meta = dalloc<int2>(c, meta.size());
         S.ci = dalloc<int>(c, ci.size());
@@ -384,7 +404,7 @@ double alg_bytes(const DMat& M) {
 }
 
 std::string fmt_name(const DMat& M) {
-    return M.fmt == 1 ? "sbsr3" : M.fmt == 2 ? (M.sell.perm ? "sells" : "sell") : "csr" + std::to_string(M.csr.group);
+    return M.fmt == 1 ? "sbsr3" : M.fmt == 2 ? (M.sell.perm ? "sells" : M.sell.chh == 8 ? "sell8" : "sell") : "csr" + std::to_string(M.csr.group);
 }
 
 void add_spmv(aspamg_gpu_ctx* c, std::vector<Op>& ops, const std::string& name, int level, const DMat& M, Epi epi,
@@ -815,6 +835,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "sell_sort_fill_pct") c->opt_sell_sort_fill_pct = value;
         else if (k == "sell_u") c->opt_sell_u = value;
         else if (k == "sell_tma") c->opt_sell_tma = value;
+        else if (k == "sell_chh") c->opt_sell_chh = value;
         else if (k == "pdl") set_pdl(value != 0);
         else if (k == "coarse_mode") c->opt_coarse_mode = (int)value;
         else throw Fail{4, "set_option: unknown key " + k};

@@ -358,14 +358,17 @@ struct SellChunk {
 template <int STREAM>
 __device__ __forceinline__ SellChunk sell_chunk(const DSell& M, int ch, int lane, bool need_aux, const double* aux,
                                                 const double* dotw) {
+    // ch = group of 32 slot rows (one warp); the layout's chunk height chh (8 or
+    // 32) splits the group into 32/chh chunks, each with its own width/offset.
     SellChunk c;
     const int srow = ch * 32 + lane;
     c.act = srow < M.n_rows;
     c.len = c.act ? __ldg(M.len + srow) : 0;
     c.row = c.act ? (M.perm ? __ldg(M.perm + srow) : srow) : 0;
-    const int2 mw = __ldg(M.meta + ch);
-    c.w = mw.y;
-    c.base = (long long)mw.x * 32 + lane;
+    const int sub = min(srow, M.n_rows - 1) / M.chh;
+    const int2 mw = __ldg(M.meta + sub);
+    c.w = M.chh == 32 ? mw.y : (int)__reduce_max_sync(0xffffffffu, (unsigned)mw.y);
+    c.base = (long long)mw.x * M.chh + (srow % M.chh);
     c.av = (c.act && need_aux) ? aux[c.row] : 0.0;
     c.dw = (c.act && dotw) ? dotw[c.row] : 0.0;
     return c;
@@ -381,6 +384,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const d
     const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * kBlock) >> 5;
     const bool need_aux = epi == EPI_RESID || epi == EPI_ADD || epi == EPI_ADDSCALE;
+    const long long SS = M.chh;  // slot stride
     double dacc = 0.0;
     int ch = warp;
     SellChunk nx{};
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const d
     if (ch < M.nchunks) {
         nx = sell_chunk<STREAM>(M, ch, lane, need_aux, aux, dotw);
 #pragma unroll
-        for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? ld_mat<STREAM>(M.ci + nx.base + 32ll * u) : 0;
+        for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? ld_mat<STREAM>(M.ci + nx.base + SS * u) : 0;
     }
     while (ch < M.nchunks) {
         const SellChunk cu = nx;
@@ -404,16 +408,16 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const d
             for (int u = 0; u < U; ++u) {
                 cc[u] = cn[u];
                 const bool p = j0 + u < cu.len;
-                v[u] = p ? ld_mat<STREAM>(M.v + cu.base + 32ll * (j0 + u)) : 0.0;
+                v[u] = p ? ld_mat<STREAM>(M.v + cu.base + SS * (j0 + u)) : 0.0;
                 xv[u] = p ? __ldg(x + cc[u]) : 0.0;
             }
             if (j0 + U < cu.w) {
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    cn[u] = (j0 + U + u < cu.len) ? ld_mat<STREAM>(M.ci + cu.base + 32ll * (j0 + U + u)) : 0;
+                    cn[u] = (j0 + U + u < cu.len) ? ld_mat<STREAM>(M.ci + cu.base + SS * (j0 + U + u)) : 0;
             } else if (chn < M.nchunks) {
 #pragma unroll
-                for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? ld_mat<STREAM>(M.ci + nx.base + 32ll * u) : 0;
+                for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? ld_mat<STREAM>(M.ci + nx.base + SS * u) : 0;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u)

@@ -51,6 +51,7 @@ struct DSbsr3 {
 struct DSell {
     int n_rows = 0, n_cols = 0, nchunks = 0;
     long long nnz = 0, slots = 0;
+    int chh = 32;         // chunk height: 32 (one chunk per warp) or 8 (four chunks per warp)
     int* perm = nullptr;  // SELL-32-sigma: slot row -> matrix row (null = natural order)
     int* len = nullptr;   // per slot row
     int u = 81;           // register-pipelined variant: U*10 + min CTAs/SM (81, 83, 84, 41, 44, 46, 21)
