@@ -16,7 +16,7 @@ CXX      := /usr/bin/g++
 # Portable x86-64 baseline: the GPU box's host CPU is not this container's.
 CXXFLAGS := -std=c++20 -O3 -march=x86-64-v2 -ffp-contract=off -fPIC -fopenmp -Wall -Wextra
 NVFLAGS  := -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a \
-            -ccbin /usr/bin/g++ -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+            -ccbin /usr/bin/g++ -Xcompiler -fPIC -Xcompiler -fopenmp -Xptxas -v --expt-relaxed-constexpr
 
 all: $(LIB)/libaspamg_host.so $(LIB)/libaspamg_gpu.so oracle
 
@@ -26,7 +26,7 @@ $(LIB)/libaspamg_host.so: $(HOSTSRC) $(HOSTHDR)
 
 $(LIB)/libaspamg_gpu.so: $(GPUSRC) $(GPUHDR)
 	@mkdir -p $(LIB)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPUSRC) 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPUSRC) -lgomp 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
 
 oracle:
 	$(MAKE) -C oracle

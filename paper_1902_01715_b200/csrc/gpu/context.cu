@@ -74,7 +74,7 @@ struct aspamg_gpu_ctx {
     int opt_bsr = 1, opt_device_loop = 1, opt_coarse_mode = 1;
     long long opt_sell_min_rows = 65536, opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
               opt_sell_u = 0, opt_sell_tma = 0, opt_sell_chh = 0;
-    long long opt_stream_bytes = 48ll << 20, opt_keep_bytes = 64ll << 20, opt_tail_rows = 0;
+    long long opt_stream_bytes = 48ll << 20, opt_keep_bytes = 64ll << 20, opt_tail_rows = 0, opt_csr_per_thread = 4;
     // PCG state and vectors
     PcgState* st = nullptr;       // device
     PcgState* st_host = nullptr;  // pinned
@@ -167,21 +167,25 @@ bool exact_bsr3(const aspamg_csr_view& v) {
     if (v.n_rows % 3 || v.n_cols % 3 || v.n_rows == 0) return false;
     const int64_t* rp = v.row_offsets;
     const int64_t* ci = v.col_indices;
-    for (int64_t br = 0; br < v.n_rows / 3; ++br) {
+    const int64_t nb = v.n_rows / 3;
+    int ok = 1;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+    for (int64_t br = 0; br < nb; ++br) {
         const int64_t r0 = 3 * br;
         const int64_t len = rp[r0 + 1] - rp[r0];
-        if (len % 3) return false;
-        for (int k = 1; k < 3; ++k)
-            if (rp[r0 + k + 1] - rp[r0 + k] != len) return false;
-        for (int64_t t = 0; t < len; t += 3) {
+        bool good = len % 3 == 0;
+        for (int k = 1; k < 3 && good; ++k)
+            if (rp[r0 + k + 1] - rp[r0 + k] != len) good = false;
+        for (int64_t t = 0; t < len && good; t += 3) {
             const int64_t c0 = ci[rp[r0] + t];
-            if (c0 % 3) return false;
-            for (int k = 0; k < 3; ++k)
+            if (c0 % 3) good = false;
+            for (int k = 0; k < 3 && good; ++k)
                 for (int cc = 0; cc < 3; ++cc)
-                    if (ci[rp[r0 + k] + t + cc] != c0 + cc) return false;
+                    if (ci[rp[r0 + k] + t + cc] != c0 + cc) good = false;
         }
+        ok = ok && good;
     }
-    return true;
+    return ok != 0;
 }
 
 void check_view(const aspamg_csr_view* v, const char* what) {
@@ -191,9 +195,11 @@ void check_view(const aspamg_csr_view* v, const char* what) {
     if (v->n_rows > 0 && v->row_offsets[v->n_rows] != v->nnz) throw Fail{1, std::string(what) + ": nnz mismatch"};
     if (v->nnz >= (1ll << 31) || v->n_rows >= (1ll << 31) || v->n_cols >= (1ll << 31))
         throw Fail{4, std::string(what) + ": exceeds int32 device indexing"};
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
     for (int64_t k = 0; k < v->nnz; ++k)
-        if (v->col_indices[k] < 0 || v->col_indices[k] >= v->n_cols)
-            throw Fail{1, std::string(what) + ": column index out of range"};
+        bad |= (v->col_indices[k] < 0 || v->col_indices[k] >= v->n_cols);
+    if (bad) throw Fail{1, std::string(what) + ": column index out of range"};
 }
 
 // Threads per row for the CSR kernel: ~4+ entries per thread, widened for
@@ -206,9 +212,9 @@ void check_view(const aspamg_csr_view* v, const char* what) {
 // on small operands (< 64k rows, where the longest row's serial chain sets the
 // kernel latency) also <= ~32 sequential entries for the longest row, and
 // widened so the grid still covers the GPU (>= ~150k threads).
-int group_for(double mean, int maxlen, int64_t n_rows) {
+int group_for(double mean, int maxlen, int64_t n_rows, double per_thread = 4.0) {
     int g = 1;
-    while (g < 256 && 4.0 * 2 * g <= mean) g *= 2;
+    while (g < 256 && per_thread * 2 * g <= mean) g *= 2;
     if (n_rows < 65536)
         while (g < 256 && 32 * g < maxlen) g *= 2;
     while (g < 256 && (double)n_rows * g < 150000.0 && 2.0 * g <= std::max(mean, 1.0)) g *= 2;
@@ -253,6 +259,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         slice_meta(len, meta, B.slots);
         std::vector<int> ci((size_t)B.slots * 32, 0);
         std::vector<double> val((size_t)B.slots * 288, 0.0);
+#pragma omp parallel for schedule(static)
         for (int br = 0; br < B.nb; ++br) {
             const int ch = br / 32, lane = br % 32;
             const long long off = meta[(size_t)ch].x;
@@ -324,6 +331,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         // S.slots counts slot rows of h entries; store padded entries / 32 for the byte accounting
         std::vector<int> ci((size_t)std::max<long long>(S.slots * h, 1), 0);
         std::vector<double> val(ci.size(), 0.0);
+#pragma omp parallel for schedule(static)
         for (int64_t sr = 0; sr < v.n_rows; ++sr) {
             const int64_t i = perm.empty() ? sr : perm[(size_t)sr];
             const long long off = meta[(size_t)(sr / h)].x;
@@ -359,6 +367,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     A.nnz = nnz;
     std::vector<int> rp((size_t)v.n_rows + 1), ci((size_t)nnz);
     for (int64_t i = 0; i <= v.n_rows; ++i) rp[(size_t)i] = (int)(v.n_rows ? v.row_offsets[i] : 0);
+#pragma omp parallel for schedule(static)
     for (int64_t k = 0; k < nnz; ++k) ci[(size_t)k] = (int)v.col_indices[k];
     A.rp = dalloc<int>(c, rp.size());
     A.ci = dalloc<int>(c, ci.size());
@@ -368,7 +377,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         CK(cudaMemcpy(A.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(A.v, v.values, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice));
     }
-    A.group = group_for(mean, maxlen, v.n_rows);
+    A.group = group_for(mean, maxlen, v.n_rows, (double)c->opt_csr_per_thread);
     A.pol = (long long)(12.0 * nnz) > c->opt_stream_bytes ? 1 : 0;
     return M;
 }
@@ -828,6 +837,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "stream_bytes") c->opt_stream_bytes = value;
         else if (k == "keep_bytes") c->opt_keep_bytes = value;
         else if (k == "tail_rows") c->opt_tail_rows = value;
+        else if (k == "csr_per_thread") c->opt_csr_per_thread = std::max<int64_t>(1, value);
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;
         else if (k == "sell_max_len") c->opt_sell_max_len = value;
         else if (k == "sell_min_rows") c->opt_sell_min_rows = value;
