@@ -81,6 +81,14 @@ class Dist:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum(self, v: float) -> float:
+        if self.ws == 1:
+            return v
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
     def close(self):
         if self.ws > 1:
             self.dist.destroy_process_group()
@@ -287,8 +295,11 @@ def run_b200(args, ws, rank, local):
         per_solve.append((ms, it, cv, tr))
     clocks = clk.stop()
     dist.barrier()
+    # whole job: slowest rank's device time over the PCG iterations of ALL ranks
+    # (replicas: every rank solves its own copy; N ranks do N x the iterations)
     tot_ms = dist.max(tot_ms)
-    value = (tot_ms / 1e3) / max(tot_it, 1)
+    job_it = dist.sum(float(tot_it))
+    value = (tot_ms / 1e3) / max(job_it, 1.0)
     n_iters = per_solve[-1][1]
     converged = all(p[2] for p in per_solve)
 
@@ -315,7 +326,7 @@ def run_b200(args, ws, rank, local):
             e2e_t += dt
             e2e_it += int(n_it.value)
     e2e_t = dist.max(e2e_t)
-    e2e_value = e2e_t / max(e2e_it, 1)
+    e2e_value = e2e_t / max(dist.sum(float(e2e_it)), 1.0)
     x_host = np.ctypeslib.as_array(xp, shape=(n,)).copy()
     lib.aspamg_gpu_free_pinned(pin_b)
     lib.aspamg_gpu_free_pinned(pin_x)

@@ -35,7 +35,8 @@ def _worker(rank, ws, port, cache_root, q):
     import pyoracle as O
     st, x, hist, conv, trr = O.OracleHierarchy(h).pcg(prob.rhs)
     t = d.max(float(rank + 1))
-    q.put((rank, chk, len(hist), conv, t))
+    tot = d.sum(float(len(hist)))
+    q.put((rank, chk, len(hist), conv, t, tot))
     d.close()
 
 
@@ -52,7 +53,8 @@ def test_two_rank_replicas_gloo(tmp_path):
         p.join(240)
         assert p.exitcode == 0
     res = sorted(q.get(timeout=10) for _ in range(2))
-    (_, c0, n0, v0, t0), (_, c1, n1, v1, t1) = res
+    (_, c0, n0, v0, t0, s0), (_, c1, n1, v1, t1, s1) = res
     assert c0 == c1 and n0 == n1 and v0 and v1
     assert t0 == t1 == 2.0  # max over ranks
+    assert s0 == s1 == 2.0 * n0  # whole-job iterations (replicas)
     assert any(f.startswith("hier_c1_s4") for f in os.listdir(tmp_path / ".cache"))
