@@ -43,8 +43,7 @@ bool chol_append(const Csr& A, RowWork& w, const std::vector<index_t>& pat, int 
     for (index_t k = A.row_begin(j); k < A.row_end(j); ++k)
         w.dense[static_cast<size_t>(A.col[static_cast<size_t>(k)])] = 0.0;
     trsv_lower(m, w.L.data(), w.cap, row);
-    double d = ajj;
-    for (int q = 0; q < m; ++q) d -= row[q] * row[q];
+    const double d = ajj - dot_fixed4(row, row, m);
     if (!(d > 0.0)) return false;
     row[m] = std::sqrt(d);
     return true;
@@ -100,8 +99,7 @@ Csr afsai_build(const Csr& A, const Csr* G_start, index_t k, index_t rho, double
                 std::vector<double> a(y);
                 trsv_lower(m, w.L.data(), w.cap, y.data());
                 trsv_lower_t(m, w.L.data(), w.cap, y.data());
-                psi = aii;
-                for (int q = 0; q < m; ++q) psi -= a[static_cast<size_t>(q)] * y[static_cast<size_t>(q)];
+                psi = aii - dot_fixed4(a.data(), y.data(), m);
                 if (!(psi > 0.0)) { ok = false; break; }
                 if (step > 0 && (psi_prev - psi) <= eps * psi_prev) break;  // (c)
                 if (step == k) break;

@@ -23,12 +23,26 @@ long cholesky_lower(int n, double* a) {
     return -1;
 }
 
-void trsv_lower(int n, const double* L, int ld, double* b) {
-    for (int i = 0; i < n; ++i) {
-        double s = b[i];
-        for (int k = 0; k < i; ++k) s -= L[i * ld + k] * b[k];
-        b[i] = s / L[i * ld + i];
+// Four independent partial sums (fixed order, combined pairwise) break the
+// dependent add chain of the row dot product: same result for every run and
+// thread count, ~4x the throughput of a single accumulator.
+static inline double dot4(const double* a, const double* b, int n) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int k = 0;
+    for (; k + 4 <= n; k += 4) {
+        s0 += a[k] * b[k];
+        s1 += a[k + 1] * b[k + 1];
+        s2 += a[k + 2] * b[k + 2];
+        s3 += a[k + 3] * b[k + 3];
     }
+    for (; k < n; ++k) s0 += a[k] * b[k];
+    return (s0 + s1) + (s2 + s3);
+}
+
+double dot_fixed4(const double* a, const double* b, int n) { return dot4(a, b, n); }
+
+void trsv_lower(int n, const double* L, int ld, double* b) {
+    for (int i = 0; i < n; ++i) b[i] = (b[i] - dot4(L + (size_t)i * ld, b, i)) / L[i * ld + i];
 }
 
 void trsv_lower_t(int n, const double* L, int ld, double* b) {

@@ -11,6 +11,8 @@ namespace aspamg {
 // the first non-positive pivot, or -1 on success. The strict upper part is
 // zeroed.
 long cholesky_lower(int n, double* a);
+// sum_k a[k] b[k] with four fixed partial sums (deterministic).
+double dot_fixed4(const double* a, const double* b, int n);
 // Solve L y = b in place (L row-major lower, leading dimension ld).
 void trsv_lower(int n, const double* L, int ld, double* b);
 // Solve L' y = b in place.
