@@ -73,7 +73,8 @@ struct aspamg_gpu_ctx {
     // options
     int opt_bsr = 1, opt_device_loop = 1, opt_coarse_mode = 1;
     long long opt_sell_min_rows = 65536, opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
-              opt_sell_u = 0, opt_sell_tma = 0, opt_sell_chh = 0;
+              opt_sell_u = 0, opt_sell_tma = 0, opt_sell_chh = 0, opt_sell_sort = 0,
+              opt_sell_min_mean = 8;
     long long opt_stream_bytes = 48ll << 20, opt_keep_bytes = 64ll << 20, opt_tail_rows = 0, opt_csr_per_thread = 4;
     // PCG state and vectors
     PcgState* st = nullptr;       // device
@@ -288,7 +289,19 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         len[(size_t)i] = (int)(v.row_offsets[i + 1] - v.row_offsets[i]);
         maxlen = std::max(maxlen, len[(size_t)i]);
     }
-    if (v.n_rows >= c->opt_sell_min_rows && mean <= (double)c->opt_sell_max_mean && maxlen <= c->opt_sell_max_len) {
+    bool sell = v.n_rows >= c->opt_sell_min_rows && mean <= (double)c->opt_sell_max_mean &&
+                mean >= (double)c->opt_sell_min_mean && maxlen <= c->opt_sell_max_len;
+    if (sell && c->opt_sell_chh == 0 && !c->opt_sell_sort && nnz > 0) {
+        // natural order only (sorted SELL loses the x-gather locality): fall back
+        // to CSR when neither chunk height pads <= the limit
+        std::vector<int2> m32, m8;
+        long long a = 0, b = 0;
+        slice_meta(len, m32, a, 32);
+        slice_meta(len, m8, b, 8);
+        const double lim = (double)c->opt_sell_sort_fill_pct / 100.0;
+        sell = double(a) * 32.0 / double(nnz) <= lim || double(b) * 8.0 / double(nnz) <= lim;
+    }
+    if (sell) {
         M.fmt = 2;
         DSell& S = M.sell;
         S.n_rows = (int)v.n_rows;
@@ -846,6 +859,8 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "sell_u") c->opt_sell_u = value;
         else if (k == "sell_tma") c->opt_sell_tma = value;
         else if (k == "sell_chh") c->opt_sell_chh = value;
+        else if (k == "sell_sort") c->opt_sell_sort = value;
+        else if (k == "sell_min_mean") c->opt_sell_min_mean = value;
         else if (k == "pdl") set_pdl(value != 0);
         else if (k == "coarse_mode") c->opt_coarse_mode = (int)value;
         else throw Fail{4, "set_option: unknown key " + k};

@@ -273,14 +273,17 @@ def test_coarse_tail_persistent_kernel_matches_oracle(pkg, oracle, tail_rows):
 
 
 @pytest.mark.parametrize("opts", [{"sell_chh": 8}, {"sell_chh": 32, "sell_sort_fill_pct": 100000},
-                                  {"sell_sigma": 256}, {"sell_u": 41}, {"sell_u": 21},
+                                  {"sell_sort": 1}, {"sell_sort": 1, "sell_sigma": 256}, {"sell_u": 41}, {"sell_u": 21},
                                   {"sell_tma": 164}, {"sell_tma": 82}, {"pdl": 0}])
 def test_sell_layout_variants_are_bit_identical(pkg, opts):
     """Every SELL layout/kernel variant sums each row sequentially in ascending
     column order, so the V-cycle output is bit-identical across variants."""
     p, h = problem_and_hierarchy(2, 2)
     y = np.random.default_rng(5).standard_normal(p.K.n_rows)
-    ref = _gpu(pkg, h).apply(y)
+    ref = _gpu(pkg, h, sell_chh=32, sell_sort_fill_pct=100000, sell_min_mean=1).apply(y)
+    opts = dict(opts, sell_min_mean=1)
+    if "sell_sort" not in opts:  # keep every SELL-eligible operand in SELL (CSR trees differ in bits)
+        opts.setdefault("sell_sort_fill_pct", 100000)
     g = _gpu(pkg, h, **opts)
     assert np.array_equal(g.apply(y), ref)
     if "pdl" in opts:
