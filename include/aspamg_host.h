@@ -80,6 +80,21 @@ int aspamg_problem_coords(const aspamg_problem* p, const double** xyz, int64_t* 
 void aspamg_problem_free(aspamg_problem* p);
 
 int aspamg_setup_config_default(aspamg_setup_config* cfg);
+/* Setup components exposed for verification (SPEC.md operations):
+ * SRQCG (Alg. 4) on S = G A G' from V0 (n x m column-major); writes V (n x m_out,
+ * orthonormal columns, ascending quotients), quotients[m_out], m_out. */
+int aspamg_srqcg(const aspamg_csr_view* A, const aspamg_csr_view* G, const double* V0, int64_t m,
+                 int64_t k_max, int64_t k_ritz, double tol, uint64_t seed, double* V, double* quotients,
+                 int64_t* m_out);
+/* aFSAI build from the identity start: returns G via a new hierarchy-owned
+ * buffer set; G_out views stay valid until aspamg_csr_free. */
+typedef struct aspamg_csr_owned aspamg_csr_owned;
+int aspamg_afsai_build(const aspamg_csr_view* A, int64_t k, int64_t rho, double eps, aspamg_csr_owned** G,
+                       aspamg_csr_view* G_view);
+/* Lanczos estimate of lambda_max(G A G') x 1.05. */
+int aspamg_estimate_lambda_max(const aspamg_csr_view* G, const aspamg_csr_view* A, int64_t steps, uint64_t seed,
+                               double* lambda_hat);
+void aspamg_csr_free(aspamg_csr_owned* m);
 /* coords: n_nodes x 3 row-major free-node coordinates (3 dofs per node,
  * interleaved) or NULL; drives the rigid-body-mode seeding of the test space. */
 int aspamg_setup(const aspamg_csr_view* A, const double* coords, int64_t n_nodes,

@@ -16,6 +16,9 @@ struct aspamg_problem {
 struct aspamg_hierarchy {
     Hierarchy h;
 };
+struct aspamg_csr_owned {
+    Csr m;
+};
 
 namespace {
 thread_local std::string g_err;
@@ -197,5 +200,43 @@ int aspamg_hierarchy_load(const char* path, aspamg_hierarchy** out) {
 }
 
 void aspamg_hierarchy_free(aspamg_hierarchy* h) { delete h; }
+
+int aspamg_srqcg(const aspamg_csr_view* A, const aspamg_csr_view* G, const double* V0, int64_t m, int64_t k_max,
+                 int64_t k_ritz, double tol, uint64_t seed, double* V, double* quotients, int64_t* m_out) {
+    return guard([&] {
+        Csr a = from_view(*A), g = from_view(*G);
+        Csr gt = transpose(g);
+        Dense v0(a.n_rows, m);
+        std::copy(V0, V0 + a.n_rows * m, v0.v.begin());
+        SrqcgConfig cfg;
+        cfg.n_tv = m; cfg.k_max = k_max; cfg.k_ritz = k_ritz; cfg.residual_tol = tol; cfg.seed = seed;
+        TestSpace ts = srqcg(a, g, gt, v0, cfg);
+        std::copy(ts.V.v.begin(), ts.V.v.end(), V);
+        std::copy(ts.quotients.begin(), ts.quotients.end(), quotients);
+        *m_out = ts.V.n_cols;
+    });
+}
+
+int aspamg_afsai_build(const aspamg_csr_view* A, int64_t k, int64_t rho, double eps, aspamg_csr_owned** G,
+                       aspamg_csr_view* G_view) {
+    return guard([&] {
+        Csr a = from_view(*A);
+        auto* o = new aspamg_csr_owned;
+        try { o->m = afsai_build(a, nullptr, k, rho, eps); } catch (...) { delete o; throw; }
+        *G = o;
+        *G_view = view(o->m);
+    });
+}
+
+int aspamg_estimate_lambda_max(const aspamg_csr_view* G, const aspamg_csr_view* A, int64_t steps, uint64_t seed,
+                               double* lambda_hat) {
+    return guard([&] {
+        Csr g = from_view(*G), a = from_view(*A);
+        Csr gt = transpose(g);
+        *lambda_hat = estimate_lambda_max(g, gt, a, steps, seed);
+    });
+}
+
+void aspamg_csr_free(aspamg_csr_owned* m) { delete m; }
 
 }  // extern "C"

@@ -104,63 +104,61 @@ TestSpace srqcg(const Csr& A, const Csr& G, const Csr& Gt, const Dense& V0, cons
     std::vector<double> gi(static_cast<size_t>(n));
     for (index_t k = 1; !all_conv && cfg.k_max > 0; ++k) {
         if (cfg.k_ritz > 0 && k % cfg.k_ritz == 0) {
-            // Ritz: (Z'SZ) U = (Z'Z) U Lambda ; Z <- Z U, SZ <- SZ U.
+            // Ritz projection (ZᵀSZ) U = (ZᵀZ) U Λ, Z <- Z U. Solved on an orthonormal
+            // basis of span(Z): two-pass MGS of Z with the same column operations on
+            // SZ (SZ stays S·Z without new S products); a column that collapses (the
+            // per-vector minimisations drifting onto one eigenvector) is replaced by a
+            // seeded random vector — the same rank-collapse rule as the entry step.
             const int m = static_cast<int>(nt);
-            std::vector<double> M1(static_cast<size_t>(m) * m), M2(static_cast<size_t>(m) * m);
-            for (int a = 0; a < m; ++a)
-                for (int b = 0; b <= a; ++b) {
-                    M1[static_cast<size_t>(a) * m + b] = M1[static_cast<size_t>(b) * m + a] = dot(n, Z.colp(a), SZ.colp(b));
-                    M2[static_cast<size_t>(a) * m + b] = M2[static_cast<size_t>(b) * m + a] = dot(n, Z.colp(a), Z.colp(b));
-                }
-            for (int a = 0; a < m; ++a)  // symmetrise Z'SZ
-                for (int b = 0; b < a; ++b) {
-                    const double s = 0.5 * (M1[static_cast<size_t>(a) * m + b] + M1[static_cast<size_t>(b) * m + a]);
-                    M1[static_cast<size_t>(a) * m + b] = M1[static_cast<size_t>(b) * m + a] = s;
-                }
-            if (cholesky_lower(m, M2.data()) < 0) {
-                // C = L^{-1} M1 L^{-T}
-                std::vector<double> C(M1);
-                for (int c = 0; c < m; ++c) {  // columns: L^{-1} M1
-                    std::vector<double> col(static_cast<size_t>(m));
-                    for (int r = 0; r < m; ++r) col[static_cast<size_t>(r)] = C[static_cast<size_t>(r) * m + c];
-                    trsv_lower(m, M2.data(), m, col.data());
-                    for (int r = 0; r < m; ++r) C[static_cast<size_t>(r) * m + c] = col[static_cast<size_t>(r)];
-                }
-                for (int r = 0; r < m; ++r) {  // rows: (.) L^{-T}
-                    std::vector<double> row(C.begin() + r * m, C.begin() + (r + 1) * m);
-                    trsv_lower(m, M2.data(), m, row.data());
-                    std::copy(row.begin(), row.end(), C.begin() + r * m);
-                }
-                for (int a = 0; a < m; ++a)
-                    for (int b = 0; b < a; ++b) {
-                        const double s = 0.5 * (C[static_cast<size_t>(a) * m + b] + C[static_cast<size_t>(b) * m + a]);
-                        C[static_cast<size_t>(a) * m + b] = C[static_cast<size_t>(b) * m + a] = s;
+            for (int j = 0; j < m; ++j) {
+                double* zj = Z.colp(j);
+                double* szj = SZ.colp(j);
+                const double orig = norm2(n, zj);
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int q = 0; q < j; ++q) {
+                        const double cq = dot(n, Z.colp(q), zj);
+                        axpy(n, -cq, Z.colp(q), zj);
+                        axpy(n, -cq, SZ.colp(q), szj);
                     }
-                std::vector<double> w(static_cast<size_t>(m)), Y(static_cast<size_t>(m) * m);
-                sym_eig(m, C.data(), w.data(), Y.data());
-                // U = L^{-T} Y
-                std::vector<double> U(static_cast<size_t>(m) * m);
-                for (int c = 0; c < m; ++c) {
-                    std::vector<double> col(static_cast<size_t>(m));
-                    for (int r = 0; r < m; ++r) col[static_cast<size_t>(r)] = Y[static_cast<size_t>(r) * m + c];
-                    trsv_lower_t(m, M2.data(), m, col.data());
-                    for (int r = 0; r < m; ++r) U[static_cast<size_t>(r) * m + c] = col[static_cast<size_t>(r)];
+                double nr = norm2(n, zj);
+                if (!(nr > 1e-10 * orig)) {
+                    out.rank_collapse = true;
+                    Rng rng(derive_seed(cfg.seed, 1000 + static_cast<std::uint64_t>(k) * 64 + static_cast<std::uint64_t>(j)));
+                    for (index_t i = 0; i < n; ++i) zj[i] = rng.symmetric();
+                    for (int pass = 0; pass < 2; ++pass)
+                        for (int q = 0; q < j; ++q) axpy(n, -dot(n, Z.colp(q), zj), Z.colp(q), zj);
+                    nr = norm2(n, zj);
+                    S.apply(zj, szj);
                 }
-                Dense Zn(n, nt), SZn(n, nt);
-#pragma omp parallel for schedule(static) num_threads(num_threads())
-                for (index_t i = 0; i < n; ++i)
-                    for (int c = 0; c < m; ++c) {
-                        double s1 = 0.0, s2 = 0.0;
-                        for (int r = 0; r < m; ++r) {
-                            s1 += Z(i, r) * U[static_cast<size_t>(r) * m + c];
-                            s2 += SZ(i, r) * U[static_cast<size_t>(r) * m + c];
-                        }
-                        Zn(i, c) = s1;
-                        SZn(i, c) = s2;
-                    }
-                Z = std::move(Zn);
-                SZ = std::move(SZn);
+                const double inv = 1.0 / nr;
+#pragma omp parallel for schedule(static) num_threads(num_threads()) if (n > 65536)
+                for (index_t i = 0; i < n; ++i) {
+                    zj[i] *= inv;
+                    szj[i] *= inv;
+                }
             }
+            std::vector<double> M1(static_cast<size_t>(m) * m);
+            for (int a1 = 0; a1 < m; ++a1)
+                for (int b1 = 0; b1 <= a1; ++b1) {
+                    const double v = 0.5 * (dot(n, Z.colp(a1), SZ.colp(b1)) + dot(n, Z.colp(b1), SZ.colp(a1)));
+                    M1[static_cast<size_t>(a1) * m + b1] = M1[static_cast<size_t>(b1) * m + a1] = v;
+                }
+            std::vector<double> w(static_cast<size_t>(m)), U(static_cast<size_t>(m) * m);
+            sym_eig(m, M1.data(), w.data(), U.data());
+            Dense Zn(n, nt), SZn(n, nt);
+#pragma omp parallel for schedule(static) num_threads(num_threads())
+            for (index_t i = 0; i < n; ++i)
+                for (int c = 0; c < m; ++c) {
+                    double s1 = 0.0, s2 = 0.0;
+                    for (int r = 0; r < m; ++r) {
+                        s1 += Z(i, r) * U[static_cast<size_t>(r) * m + c];
+                        s2 += SZ(i, r) * U[static_cast<size_t>(r) * m + c];
+                    }
+                    Zn(i, c) = s1;
+                    SZn(i, c) = s2;
+                }
+            Z = std::move(Zn);
+            SZ = std::move(SZn);
         }
         all_conv = true;
         for (index_t i = 0; i < nt; ++i) {
