@@ -18,7 +18,7 @@ CXXFLAGS := -std=c++20 -O3 -march=x86-64-v2 -ffp-contract=off -fPIC -fopenmp -Wa
 NVFLAGS  := -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a \
             -ccbin /usr/bin/g++ -Xcompiler -fPIC -Xcompiler -fopenmp -Xptxas -v --expt-relaxed-constexpr
 
-all: $(LIB)/libaspamg_host.so $(LIB)/libaspamg_gpu.so oracle
+all: $(LIB)/libaspamg_host.so $(LIB)/libaspamg_gpu.so $(LIB)/aspamg_solve oracle
 
 $(LIB)/libaspamg_host.so: $(HOSTSRC) $(HOSTHDR)
 	@mkdir -p $(LIB)
@@ -28,11 +28,16 @@ $(LIB)/libaspamg_gpu.so: $(GPUSRC) $(GPUHDR)
 	@mkdir -p $(LIB)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPUSRC) -lgomp 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
 
+# C++ `solve` CLI on the C++ host API (include/aspamg_b200.hpp); finds the two
+# libraries next to itself (rpath $$ORIGIN).
+$(LIB)/aspamg_solve: $(PKG)/csrc/cli/aspamg_solve.cpp include/aspamg_b200.hpp $(LIB)/libaspamg_host.so $(LIB)/libaspamg_gpu.so
+	$(CXX) -std=c++20 -O2 -Wall -Wextra -o $@ $< -L$(LIB) -laspamg_host -laspamg_gpu -Wl,-rpath,'$$ORIGIN'
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(LIB)/*.so $(LIB)/ptxas.log
+	rm -f $(LIB)/*.so $(LIB)/ptxas.log $(LIB)/aspamg_solve
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
