@@ -16,7 +16,7 @@ CXX      := /usr/bin/g++
 # Portable x86-64 baseline: the GPU box's host CPU is not this container's.
 CXXFLAGS := -std=c++20 -O3 -march=x86-64-v2 -ffp-contract=off -fPIC -fopenmp -Wall -Wextra
 NVFLAGS  := -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a \
-            -ccbin /usr/bin/g++ -Xcompiler -fPIC -Xcompiler -fopenmp -Xptxas -v --expt-relaxed-constexpr
+            -ccbin /usr/bin/g++ -Xcompiler -fPIC -Xcompiler -fopenmp -Xcompiler -ffp-contract=off -Xptxas -v --expt-relaxed-constexpr
 
 all: $(LIB)/libaspamg_host.so $(LIB)/libaspamg_gpu.so $(LIB)/aspamg_solve oracle
 
@@ -24,9 +24,15 @@ $(LIB)/libaspamg_host.so: $(HOSTSRC) $(HOSTHDR)
 	@mkdir -p $(LIB)
 	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOSTSRC)
 
-$(LIB)/libaspamg_gpu.so: $(GPUSRC) $(GPUHDR)
+# The GPU setup (setup_gpu.cu) reuses the host's small dense eigensolver: the
+# same source and flags as the host library, symbols hidden.
+$(LIB)/obj/smalldense.o: $(PKG)/csrc/host/smalldense.cpp $(PKG)/csrc/host/smalldense.hpp
+	@mkdir -p $(LIB)/obj
+	$(CXX) $(CXXFLAGS) -fvisibility=hidden -c -o $@ $<
+
+$(LIB)/libaspamg_gpu.so: $(GPUSRC) $(GPUHDR) $(HOSTHDR) $(LIB)/obj/smalldense.o
 	@mkdir -p $(LIB)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPUSRC) -lgomp 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPUSRC) $(LIB)/obj/smalldense.o -lgomp 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
 
 # C++ `solve` CLI on the C++ host API (include/aspamg_b200.hpp); finds the two
 # libraries next to itself (rpath $$ORIGIN).
@@ -37,7 +43,7 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(LIB)/*.so $(LIB)/ptxas.log $(LIB)/aspamg_solve
+	rm -rf $(LIB)/*.so $(LIB)/ptxas.log $(LIB)/aspamg_solve $(LIB)/obj
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

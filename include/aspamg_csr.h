@@ -16,4 +16,10 @@ typedef struct aspamg_csr_view {
     const double* values;       /* nnz */
 } aspamg_csr_view;
 
+/* Output allocator for producers of a CSR whose size is known only after the
+ * product (the GPU Galerkin backend): returns 0 and n_rows + 1 / nnz / nnz
+ * writable buffers owned by `sink`. */
+typedef int (*aspamg_csr_alloc_fn)(void* sink, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                   int64_t** row_offsets, int64_t** col_indices, double** values);
+
 #endif

@@ -95,6 +95,23 @@ int aspamg_gpu_pcg_device(aspamg_gpu_ctx* ctx, const double* b_dev, const double
                           double rel_tol, int64_t max_it, double* x_dev, double* history,
                           int64_t* n_it, int* converged, double* true_rel_res);
 
+/* GPU setup: SRQCG (Alg. 4) on S = G A G' with the
+ * solve's SpMV kernels; bit-identical to the host aspamg_srqcg (same operation order).
+ * Signature = aspamg_srqcg_fn of aspamg_host.h (pass it to aspamg_set_srqcg_backend);
+ * device = (void*)(intptr_t)device_index. V0, V: n x m column-major host buffers,
+ * quotients[m]; m <= 64. Creates and destroys its own context. */
+int aspamg_gpu_srqcg(void* device, const aspamg_csr_view* A, const aspamg_csr_view* G,
+                     const aspamg_csr_view* Gt, const double* V0, int64_t m, int64_t k_max, int64_t k_ritz,
+                     double tol, uint64_t seed, double* V, double* quotients, int64_t* m_out,
+                     int64_t* iterations, int* rank_collapse);
+
+/* GPU setup: Galerkin A_c = P' (A P) with the host's summation
+ * order (bit-identical to aspamg's galerkin_triple); the result is written into buffers
+ * obtained from alloc(sink, ...). Signature = aspamg_galerkin_fn of aspamg_host.h.
+ * device = (void*)(intptr_t)device_index. */
+int aspamg_gpu_galerkin(void* device, const aspamg_csr_view* P, const aspamg_csr_view* Pt,
+                        const aspamg_csr_view* A, aspamg_csr_alloc_fn alloc, void* sink);
+
 /* measurement helpers */
 int aspamg_gpu_last_solve_ms(aspamg_gpu_ctx* ctx, double* ms);      /* device time of the last pcg */
 int aspamg_gpu_launch_count(aspamg_gpu_ctx* ctx, int64_t* n);       /* kernels launched by the last pcg */

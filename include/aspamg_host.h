@@ -86,9 +86,31 @@ int aspamg_setup_config_default(aspamg_setup_config* cfg);
 int aspamg_srqcg(const aspamg_csr_view* A, const aspamg_csr_view* G, const double* V0, int64_t m,
                  int64_t k_max, int64_t k_ritz, double tol, uint64_t seed, double* V, double* quotients,
                  int64_t* m_out);
+/* Test-space backend: when set, aspamg_setup runs the level-0
+ * SRQCG through fn instead of the CPU restatement, e.g. aspamg_gpu_srqcg from
+ * libaspamg_gpu.so with user = (void*)(intptr_t)device. Same arguments as aspamg_srqcg
+ * plus G' (explicit) and the iteration / rank-collapse outputs; fn must return 0 on
+ * success (its status is passed through otherwise). NULL restores the CPU path.
+ * Process-wide; not thread-safe against a concurrent aspamg_setup. */
+typedef int (*aspamg_srqcg_fn)(void* user, const aspamg_csr_view* A, const aspamg_csr_view* G,
+                               const aspamg_csr_view* Gt, const double* V0, int64_t m, int64_t k_max,
+                               int64_t k_ritz, double tol, uint64_t seed, double* V, double* quotients,
+                               int64_t* m_out, int64_t* iterations, int* rank_collapse);
+int aspamg_set_srqcg_backend(aspamg_srqcg_fn fn, void* user);
+typedef struct aspamg_csr_owned aspamg_csr_owned;
+/* Galerkin backend: when set, aspamg_setup forms every coarse
+ * operator A_c = P' (A P) through fn (e.g. aspamg_gpu_galerkin) instead of the CPU
+ * sparse products; fn writes the result through alloc(sink, ...). NULL restores the CPU
+ * path. Process-wide. */
+typedef int (*aspamg_galerkin_fn)(void* user, const aspamg_csr_view* P, const aspamg_csr_view* Pt,
+                                  const aspamg_csr_view* A, aspamg_csr_alloc_fn alloc, void* sink);
+int aspamg_set_galerkin_backend(aspamg_galerkin_fn fn, void* user);
+/* Host Galerkin product (the CPU restatement; exposed for verification). The result
+ * is owned by *out (free with aspamg_csr_free). */
+int aspamg_galerkin(const aspamg_csr_view* P, const aspamg_csr_view* A, aspamg_csr_owned** out,
+                    aspamg_csr_view* out_view);
 /* aFSAI build from the identity start: returns G via a new hierarchy-owned
  * buffer set; G_out views stay valid until aspamg_csr_free. */
-typedef struct aspamg_csr_owned aspamg_csr_owned;
 int aspamg_afsai_build(const aspamg_csr_view* A, int64_t k, int64_t rho, double eps, aspamg_csr_owned** G,
                        aspamg_csr_view* G_view);
 /* Lanczos estimate of lambda_max(G A G') x 1.05. */

@@ -103,6 +103,10 @@ def host() -> C.CDLL:
         lib.aspamg_estimate_lambda_max.argtypes = [C.POINTER(CsrView), C.POINTER(CsrView), i64, C.c_uint64, P_dbl]
         lib.aspamg_csr_free.argtypes = [C.c_void_p]
         lib.aspamg_csr_free.restype = None
+        lib.aspamg_set_srqcg_backend.argtypes = [C.c_void_p, C.c_void_p]
+        lib.aspamg_set_galerkin_backend.argtypes = [C.c_void_p, C.c_void_p]
+        lib.aspamg_galerkin.argtypes = [C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(C.c_void_p),
+                                        C.POINTER(CsrView)]
         _host = lib
     return _host
 
@@ -148,5 +152,12 @@ def gpu() -> C.CDLL:
         lib.aspamg_gpu_launch_count.argtypes = [vp, P_i64]
         lib.aspamg_gpu_last_solve_ms.argtypes = [vp, P_dbl]
         lib.aspamg_gpu_stream.argtypes = [vp, C.POINTER(vp)]
+        lib.aspamg_gpu_srqcg.argtypes = [vp, C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(CsrView), P_dbl, i64, i64,
+                                         i64, dbl, C.c_uint64, P_dbl, P_dbl, P_i64, P_i64, C.POINTER(C.c_int)]
+        lib.aspamg_gpu_galerkin.argtypes = [vp, C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(CsrView), vp, vp]
         _gpu = lib
     return _gpu
+
+
+# int (*)(void* sink, int64 n_rows, int64 n_cols, int64 nnz, int64** rp, int64** ci, double** v)
+CSR_ALLOC_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, i64, i64, i64, C.POINTER(P_i64), C.POINTER(P_i64), C.POINTER(P_dbl))

@@ -68,6 +68,12 @@ struct TestSpace {
 
 Dense seed_space(const Dense* rbms, index_t n_tv, index_t n, std::uint64_t seed);
 TestSpace srqcg(const Csr& A, const Csr& G, const Csr& Gt, const Dense& V0, const SrqcgConfig& cfg);  // Alg. 4
+// srqcg through the registered external backend (aspamg_set_srqcg_backend), if any.
+bool srqcg_backend_set();
+TestSpace srqcg_external(const Csr& A, const Csr& G, const Csr& Gt, const Dense& V0, const SrqcgConfig& cfg);
+// galerkin_triple through the registered external backend (aspamg_set_galerkin_backend), if any.
+bool galerkin_backend_set();
+Csr galerkin_external(const Csr& P, const Csr& Pt, const Csr& A);
 
 // --------------------------------------------------------------- coarsening
 Csr affinity_soc(const Csr& A, const Dense& V);

@@ -240,3 +240,106 @@ int aspamg_estimate_lambda_max(const aspamg_csr_view* G, const aspamg_csr_view* 
 void aspamg_csr_free(aspamg_csr_owned* m) { delete m; }
 
 }  // extern "C"
+
+// ------------------------------------------------ external test-space backend
+namespace {
+aspamg_srqcg_fn g_srqcg_fn = nullptr;
+void* g_srqcg_user = nullptr;
+}  // namespace
+
+namespace aspamg {
+
+bool srqcg_backend_set() { return g_srqcg_fn != nullptr; }
+
+TestSpace srqcg_external(const Csr& A, const Csr& G, const Csr& Gt, const Dense& V0, const SrqcgConfig& cfg) {
+    const aspamg_csr_view a = view(A), g = view(G), gt = view(Gt);
+    const index_t n = A.n_rows, m = V0.n_cols;
+    TestSpace ts;
+    ts.V = Dense(n, m);
+    ts.quotients.assign(static_cast<size_t>(m), 0.0);
+    int64_t m_out = 0, iters = 0;
+    int collapse = 0;
+    const int st = g_srqcg_fn(g_srqcg_user, &a, &g, &gt, V0.v.data(), m, cfg.k_max, cfg.k_ritz, cfg.residual_tol,
+                              cfg.seed, ts.V.v.data(), ts.quotients.data(), &m_out, &iters, &collapse);
+    if (st != 0) {
+        const std::string msg = "srqcg backend failed with status " + std::to_string(st);
+        if (st == 1) throw DimensionError(msg);
+        if (st == 3) throw NumericalError(msg);
+        if (st == 4) throw ConfigError(msg);
+        throw std::runtime_error(msg);
+    }
+    ts.V.resize_cols(m_out);
+    ts.quotients.resize(static_cast<size_t>(m_out));
+    ts.iterations = iters;
+    ts.rank_collapse = collapse != 0;
+    return ts;
+}
+
+}  // namespace aspamg
+
+int aspamg_set_srqcg_backend(aspamg_srqcg_fn fn, void* user) {
+    g_srqcg_fn = fn;
+    g_srqcg_user = user;
+    return 0;
+}
+
+// ------------------------------------------------------ external Galerkin backend
+namespace {
+aspamg_galerkin_fn g_galerkin_fn = nullptr;
+void* g_galerkin_user = nullptr;
+
+int csr_sink_alloc(void* sink, int64_t n_rows, int64_t n_cols, int64_t nnz, int64_t** rp, int64_t** ci, double** v) {
+    auto* m = static_cast<aspamg::Csr*>(sink);
+    try {
+        m->n_rows = n_rows;
+        m->n_cols = n_cols;
+        m->rowptr.assign(static_cast<size_t>(n_rows) + 1, 0);
+        m->col.assign(static_cast<size_t>(nnz), 0);
+        m->val.assign(static_cast<size_t>(nnz), 0.0);
+    } catch (...) {
+        return 5;
+    }
+    *rp = m->rowptr.data();
+    *ci = m->col.data();
+    *v = m->val.data();
+    return 0;
+}
+}  // namespace
+
+namespace aspamg {
+
+bool galerkin_backend_set() { return g_galerkin_fn != nullptr; }
+
+Csr galerkin_external(const Csr& P, const Csr& Pt, const Csr& A) {
+    const aspamg_csr_view p = view(P), pt = view(Pt), a = view(A);
+    Csr C;
+    const int st = g_galerkin_fn(g_galerkin_user, &p, &pt, &a, csr_sink_alloc, &C);
+    if (st != 0) {
+        const std::string msg = "galerkin backend failed with status " + std::to_string(st);
+        if (st == 1) throw DimensionError(msg);
+        if (st == 3) throw NumericalError(msg);
+        if (st == 4) throw ConfigError(msg);
+        throw std::runtime_error(msg);
+    }
+    C.symmetric = A.symmetric;
+    return C;
+}
+
+}  // namespace aspamg
+
+int aspamg_set_galerkin_backend(aspamg_galerkin_fn fn, void* user) {
+    g_galerkin_fn = fn;
+    g_galerkin_user = user;
+    return 0;
+}
+
+int aspamg_galerkin(const aspamg_csr_view* P, const aspamg_csr_view* A, aspamg_csr_owned** out,
+                    aspamg_csr_view* out_view) {
+    return guard([&] {
+        Csr p = from_view(*P), a = from_view(*A);
+        auto* o = new aspamg_csr_owned;
+        try { o->m = galerkin_triple(p, a); } catch (...) { delete o; throw; }
+        *out = o;
+        *out_view = view(o->m);
+    });
+}

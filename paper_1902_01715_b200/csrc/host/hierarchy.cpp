@@ -84,7 +84,8 @@ Hierarchy amg_setup(const Csr& A0, const std::vector<double>& coords, const Hier
                 have_rbm = rbm.n_cols > 0 && rbm.n_cols <= cfg.srqcg.n_tv;
             }
             Dense V0 = seed_space(have_rbm ? &rbm : nullptr, cfg.srqcg.n_tv, n, derive_seed(cfg.srqcg.seed, 6));
-            TestSpace ts = srqcg(A, L.smoother.G, L.Gt, V0, cfg.srqcg);
+            TestSpace ts = srqcg_backend_set() ? srqcg_external(A, L.smoother.G, L.Gt, V0, cfg.srqcg)
+                                              : srqcg(A, L.smoother.G, L.Gt, V0, cfg.srqcg);
             V = std::move(ts.V);
             h.t.T_ts += now_s() - t;
         }
@@ -109,7 +110,7 @@ Hierarchy amg_setup(const Csr& A0, const std::vector<double>& coords, const Hier
         L.Pt = transpose(L.P);
         h.t.T_pl += now_s() - t;
         t = now_s();
-        Csr Ac = galerkin_triple(L.P, A);
+        Csr Ac = galerkin_backend_set() ? galerkin_external(L.P, L.Pt, A) : galerkin_triple(L.P, A);
         h.t.T_rap += now_s() - t;
         // Injected, re-orthonormalised coarse test space.
         Dense Vc(split.n_coarse, V.n_cols);

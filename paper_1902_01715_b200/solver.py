@@ -190,17 +190,30 @@ class Hierarchy:
 
     @classmethod
     def setup(cls, A: SparseMatrix, coords: Optional[np.ndarray] = None, cfg: Optional[N.SetupConfig] = None,
-              threads: int = 0) -> "Hierarchy":
+              threads: int = 0, setup_device: Optional[int] = None) -> "Hierarchy":
+        """setup_device: run the GPU setup components (SRQCG) on
+        that CUDA device; None keeps the whole setup on the CPU. Both give
+        bit-identical hierarchies."""
         lib = N.host()
         lib.aspamg_host_set_threads(threads)
         cfg = cfg or default_config()
         h = C.c_void_p()
         v = A.view()
-        if coords is not None and len(coords):
-            xyz = np.ascontiguousarray(coords, dtype=np.float64)
-            _chk_host(lib.aspamg_setup(C.byref(v), _ptr(xyz, C.c_double), xyz.shape[0], C.byref(cfg), C.byref(h)))
-        else:
-            _chk_host(lib.aspamg_setup(C.byref(v), None, 0, C.byref(cfg), C.byref(h)))
+        if setup_device is not None:
+            dev = C.c_void_p(int(setup_device)) if setup_device else None
+            lib.aspamg_set_srqcg_backend(C.cast(N.gpu().aspamg_gpu_srqcg, C.c_void_p), dev)
+            lib.aspamg_set_galerkin_backend(C.cast(N.gpu().aspamg_gpu_galerkin, C.c_void_p), dev)
+        try:
+            if coords is not None and len(coords):
+                xyz = np.ascontiguousarray(coords, dtype=np.float64)
+                _chk_host(lib.aspamg_setup(C.byref(v), _ptr(xyz, C.c_double), xyz.shape[0], C.byref(cfg),
+                                           C.byref(h)))
+            else:
+                _chk_host(lib.aspamg_setup(C.byref(v), None, 0, C.byref(cfg), C.byref(h)))
+        finally:
+            if setup_device is not None:
+                lib.aspamg_set_srqcg_backend(None, None)
+                lib.aspamg_set_galerkin_backend(None, None)
         return cls(h)
 
     @classmethod
@@ -412,9 +425,79 @@ class GpuVcycle:
 
 
 def amg_setup(A: SparseMatrix, coordinates: Optional[np.ndarray] = None, cfg: Optional[N.SetupConfig] = None,
-              threads: int = 0) -> Hierarchy:
-    """SPEC.md:436-444 (CPU setup, produces the hierarchy uploaded once)."""
-    return Hierarchy.setup(A, coordinates, cfg, threads)
+              threads: int = 0, setup_device: Optional[int] = None) -> Hierarchy:
+    """SPEC.md:436-444 (produces the hierarchy uploaded once). The setup runs on
+    the CPU; with ``setup_device`` its SRQCG test-space phase and the Galerkin
+    products run on that GPU (bit-identical hierarchy)."""
+    return Hierarchy.setup(A, coordinates, cfg, threads, setup_device)
+
+
+def gpu_srqcg(A: SparseMatrix, G: SparseMatrix, V0: np.ndarray, k_max: int, k_ritz: int = 1, tol: float = 1e-2,
+              seed: int = 1234, device: int = 0, Gt: Optional[SparseMatrix] = None):
+    """SRQCG (Alg. 4) on S = G A G' on the GPU (include/aspamg_gpu.h
+    aspamg_gpu_srqcg). Returns (V, quotients, iterations, rank_collapse)."""
+    Gt = Gt if Gt is not None else SparseMatrix.from_scipy(G.to_scipy().T.tocsr())
+    n, m = V0.shape
+    v0 = np.asfortranarray(V0, dtype=np.float64).ravel(order="F")
+    V = np.empty(n * m)
+    q = np.empty(m)
+    mo, it, rc = C.c_int64(), C.c_int64(), C.c_int()
+    av, gv, gtv = A.view(), G.view(), Gt.view()
+    P = C.POINTER(C.c_double)
+    st = N.gpu().aspamg_gpu_srqcg(C.c_void_p(device) if device else None, C.byref(av), C.byref(gv), C.byref(gtv),
+                                  v0.ctypes.data_as(P), m, k_max, k_ritz, tol, seed, V.ctypes.data_as(P),
+                                  q.ctypes.data_as(P), C.byref(mo), C.byref(it), C.byref(rc))
+    if st != 0:
+        _raise(st, N.gpu().aspamg_gpu_last_error(None).decode())
+    k = mo.value
+    return V[: n * k].reshape(n, k, order="F"), q[:k], it.value, bool(rc.value)
+
+
+class _CsrSink:
+    """Numpy-owned output for aspamg_csr_alloc_fn producers."""
+
+    def __init__(self):
+        self.arrays = None
+        self.shape = None
+        self.fn = N.CSR_ALLOC_FN(self._alloc)
+
+    def _alloc(self, sink, n_rows, n_cols, nnz, rp, ci, v):
+        self.shape = (n_rows, n_cols)
+        self.arrays = (np.zeros(n_rows + 1, np.int64), np.zeros(max(nnz, 1), np.int64), np.zeros(max(nnz, 1)))
+        self.nnz = nnz
+        rp[0] = self.arrays[0].ctypes.data_as(N.P_i64)
+        ci[0] = self.arrays[1].ctypes.data_as(N.P_i64)
+        v[0] = self.arrays[2].ctypes.data_as(N.P_dbl)
+        return 0
+
+    def matrix(self) -> "SparseMatrix":
+        rp, ci, v = self.arrays
+        return SparseMatrix(self.shape[0], self.shape[1], rp, ci[: self.nnz], v[: self.nnz])
+
+
+def gpu_galerkin(P: SparseMatrix, A: SparseMatrix, device: int = 0) -> SparseMatrix:
+    """A_c = P' (A P) on the GPU (include/aspamg_gpu.h aspamg_gpu_galerkin),
+    bit-identical to the host galerkin_triple."""
+    Pt = SparseMatrix.from_scipy(P.to_scipy().T.tocsr())
+    sink = _CsrSink()
+    pv, ptv, av = P.view(), Pt.view(), A.view()
+    st = N.gpu().aspamg_gpu_galerkin(C.c_void_p(device) if device else None, C.byref(pv), C.byref(ptv), C.byref(av),
+                                     C.cast(sink.fn, C.c_void_p), None)
+    if st != 0:
+        _raise(st, N.gpu().aspamg_gpu_last_error(None).decode())
+    return sink.matrix()
+
+
+def host_galerkin(P: SparseMatrix, A: SparseMatrix) -> SparseMatrix:
+    """The host restatement of galerkin_triple (sparse_matrix.cpp:191-199)."""
+    pv, av = P.view(), A.view()
+    h = C.c_void_p()
+    out = N.CsrView()
+    _chk_host(N.host().aspamg_galerkin(C.byref(pv), C.byref(av), C.byref(h), C.byref(out)))
+    try:
+        return SparseMatrix.from_view(out, True)
+    finally:
+        N.host().aspamg_csr_free(h)
 
 
 def vcycle_apply(h: GpuVcycle, y: np.ndarray) -> np.ndarray:
