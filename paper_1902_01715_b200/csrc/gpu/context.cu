@@ -102,6 +102,17 @@ void slice_meta(const std::vector<int>& len, std::vector<int2>& meta, long long&
     }
 }
 
+// True when every row's columns fit in [first, first + 65535] (sorted rows).
+bool rows_fit_u16(const aspamg_csr_view& v) {
+    int ok = 1;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+    for (int64_t i = 0; i < v.n_rows; ++i) {
+        const int64_t b = v.row_offsets[i], e = v.row_offsets[i + 1];
+        if (e > b && v.col_indices[e - 1] - v.col_indices[b] > 65535) ok = 0;
+    }
+    return ok != 0;
+}
+
 DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     DMat M;
     const long long nnz = v.nnz;
@@ -203,27 +214,41 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         }
         S.chh = h;
         // S.slots counts slot rows of h entries; store padded entries / 32 for the byte accounting
-        std::vector<int> ci((size_t)std::max<long long>(S.slots * h, 1), 0);
-        std::vector<double> val(ci.size(), 0.0);
+        const bool i16 = c->opt_idx16 && !c->opt_sell_tma && rows_fit_u16(v);
+        const size_t nslot = (size_t)std::max<long long>(S.slots * h, 1);
+        std::vector<int> ci(i16 ? 0 : nslot, 0), cb(i16 ? (size_t)std::max<int64_t>(v.n_rows, 1) : 0, 0);
+        std::vector<unsigned short> c16(i16 ? nslot : 0, 0);
+        std::vector<double> val(nslot, 0.0);
 #pragma omp parallel for schedule(static)
         for (int64_t sr = 0; sr < v.n_rows; ++sr) {
             const int64_t i = perm.empty() ? sr : perm[(size_t)sr];
             const long long off = meta[(size_t)(sr / h)].x;
             const int r = (int)(sr % h);
-            for (int64_t k = v.row_offsets[i]; k < v.row_offsets[i + 1]; ++k) {
-                const long long j = k - v.row_offsets[i];
-                ci[(size_t)((off + j) * h + r)] = (int)v.col_indices[k];
+            const int64_t b = v.row_offsets[i];
+            const int64_t base = (i16 && v.row_offsets[i + 1] > b) ? v.col_indices[b] : 0;
+            if (i16) cb[(size_t)sr] = (int)base;
+            for (int64_t k = b; k < v.row_offsets[i + 1]; ++k) {
+                const long long j = k - b;
+                if (i16) c16[(size_t)((off + j) * h + r)] = (unsigned short)(v.col_indices[k] - base);
+                else ci[(size_t)((off + j) * h + r)] = (int)v.col_indices[k];
                 val[(size_t)((off + j) * h + r)] = v.values[k];
             }
         }
         S.slots = (S.slots * h + 31) / 32;  // padded entries / 32 (byte accounting, as for SELL-32)
         S.len = dalloc<int>(c, slen.size());
         S.meta = dalloc<int2>(c, meta.size());
-        S.ci = dalloc<int>(c, ci.size());
         S.v = dalloc<double>(c, val.size());
         CK(cudaMemcpy(S.len, slen.data(), slen.size() * sizeof(int), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(S.meta, meta.data(), meta.size() * sizeof(int2), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(S.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
+        if (i16) {
+            S.ci16 = dalloc<unsigned short>(c, c16.size());
+            S.cb = dalloc<int>(c, cb.size());
+            CK(cudaMemcpy(S.ci16, c16.data(), c16.size() * sizeof(unsigned short), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(S.cb, cb.data(), cb.size() * sizeof(int), cudaMemcpyHostToDevice));
+        } else {
+            S.ci = dalloc<int>(c, ci.size());
+            CK(cudaMemcpy(S.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
+        }
         CK(cudaMemcpy(S.v, val.data(), val.size() * sizeof(double), cudaMemcpyHostToDevice));
         if (!perm.empty()) {
             S.perm = dalloc<int>(c, perm.size());
@@ -239,18 +264,35 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     A.n_rows = (int)v.n_rows;
     A.n_cols = (int)v.n_cols;
     A.nnz = nnz;
-    std::vector<int> rp((size_t)v.n_rows + 1), ci((size_t)nnz);
+    const bool i16 = c->opt_idx16 && rows_fit_u16(v);
+    std::vector<int> rp((size_t)v.n_rows + 1), ci(i16 ? 0 : (size_t)nnz), cb(i16 ? (size_t)std::max<int64_t>(v.n_rows, 1) : 0);
+    std::vector<unsigned short> c16(i16 ? (size_t)nnz : 0);
     for (int64_t i = 0; i <= v.n_rows; ++i) rp[(size_t)i] = (int)(v.n_rows ? v.row_offsets[i] : 0);
+    if (i16) {
 #pragma omp parallel for schedule(static)
-    for (int64_t k = 0; k < nnz; ++k) ci[(size_t)k] = (int)v.col_indices[k];
+        for (int64_t i = 0; i < v.n_rows; ++i) {
+            const int64_t b = v.row_offsets[i], e = v.row_offsets[i + 1];
+            const int64_t base = e > b ? v.col_indices[b] : 0;
+            cb[(size_t)i] = (int)base;
+            for (int64_t k = b; k < e; ++k) c16[(size_t)k] = (unsigned short)(v.col_indices[k] - base);
+        }
+    } else {
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < nnz; ++k) ci[(size_t)k] = (int)v.col_indices[k];
+    }
     A.rp = dalloc<int>(c, rp.size());
-    A.ci = dalloc<int>(c, ci.size());
     A.v = dalloc<double>(c, (size_t)nnz);
     CK(cudaMemcpy(A.rp, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice));
-    if (nnz) {
-        CK(cudaMemcpy(A.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(A.v, v.values, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice));
+    if (i16) {
+        A.ci16 = dalloc<unsigned short>(c, std::max<size_t>(c16.size(), 1));
+        A.cb = dalloc<int>(c, cb.size());
+        if (nnz) CK(cudaMemcpy(A.ci16, c16.data(), c16.size() * sizeof(unsigned short), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(A.cb, cb.data(), cb.size() * sizeof(int), cudaMemcpyHostToDevice));
+    } else {
+        A.ci = dalloc<int>(c, std::max<size_t>(ci.size(), 1));
+        if (nnz) CK(cudaMemcpy(A.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
+    if (nnz) CK(cudaMemcpy(A.v, v.values, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice));
     A.group = group_for(mean, maxlen, v.n_rows, (double)c->opt_csr_per_thread);
     A.pol = (long long)(12.0 * nnz) > c->opt_stream_bytes ? 1 : 0;
     return M;
@@ -259,8 +301,8 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
 // Device bytes of an operand's matrix stream (what one product reads).
 double mat_bytes(const DMat& M) {
     if (M.fmt == 1) return 76.0 * 32.0 * double(M.sb.slots) + 4.0 * M.sb.nb;
-    if (M.fmt == 2) return 12.0 * 32.0 * double(M.sell.slots) + 4.0 * M.sell.n_rows;
-    return 12.0 * double(M.csr.nnz) + 4.0 * (M.csr.n_rows + 1);
+    if (M.fmt == 2) return (M.sell.ci16 ? 10.0 : 12.0) * 32.0 * double(M.sell.slots) + (M.sell.ci16 ? 8.0 : 4.0) * M.sell.n_rows;
+    return (M.csr.ci16 ? 10.0 : 12.0) * double(M.csr.nnz) + 4.0 * (M.csr.n_rows + 1) + (M.csr.ci16 ? 4.0 * M.csr.n_rows : 0.0);
 }
 void set_pol(DMat& M, int pol) {
     if (M.fmt == 1) M.sb.pol = pol;
@@ -283,11 +325,18 @@ double alg_bytes(const DMat& M) {
         return 72.0 * nnzb + 4.0 * nnzb + 4.0 * (M.sb.nb + 1) + 8.0 * M.cols() + 8.0 * M.rows();
     }
     const double nnz = double(M.fmt == 2 ? M.sell.nnz : M.csr.nnz);
-    return 8.0 * nnz + 4.0 * nnz + 4.0 * (M.rows() + 1) + 8.0 * M.cols() + 8.0 * M.rows();
+    const bool i16 = M.fmt == 2 ? M.sell.ci16 != nullptr : M.csr.ci16 != nullptr;
+    // 16-bit offsets: 2 B per entry + a 4-B base column per row
+    const double idx = i16 ? 2.0 * nnz + 4.0 * M.rows() : 4.0 * nnz;
+    return 8.0 * nnz + idx + 4.0 * (M.rows() + 1) + 8.0 * M.cols() + 8.0 * M.rows();
 }
 
 std::string fmt_name(const DMat& M) {
-    return M.fmt == 1 ? "sbsr3" : M.fmt == 2 ? (M.sell.perm ? "sells" : M.sell.chh == 8 ? "sell8" : "sell") : "csr" + std::to_string(M.csr.group);
+    const bool h = M.fmt == 2 ? M.sell.ci16 != nullptr : M.fmt == 0 && M.csr.ci16 != nullptr;
+    const std::string base = M.fmt == 1   ? "sbsr3"
+                             : M.fmt == 2 ? (M.sell.perm ? "sells" : M.sell.chh == 8 ? "sell8" : "sell")
+                                          : "csr" + std::to_string(M.csr.group);
+    return h ? base + "h" : base;  // h: 16-bit column offsets
 }
 
 void add_spmv(aspamg_gpu_ctx* c, std::vector<Op>& ops, const std::string& name, int level, const DMat& M, Epi epi,
@@ -712,6 +761,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "keep_bytes") c->opt_keep_bytes = value;
         else if (k == "tail_rows") c->opt_tail_rows = value;
         else if (k == "csr_per_thread") c->opt_csr_per_thread = std::max<int64_t>(1, value);
+        else if (k == "idx16") c->opt_idx16 = value;
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;
         else if (k == "sell_max_len") c->opt_sell_max_len = value;
         else if (k == "sell_min_rows") c->opt_sell_min_rows = value;

@@ -165,6 +165,11 @@ __device__ __forceinline__ int ld_keep(const int* p) {
     asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(l2_keep_policy()));
     return r;
 }
+__device__ __forceinline__ unsigned short ld_keep(const unsigned short* p) {
+    unsigned short r;
+    asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(r) : "l"(p), "l"(l2_keep_policy()));
+    return r;
+}
 template <int POL, class T>
 __device__ __forceinline__ T ld_mat(const T* p) {
     if constexpr (POL == 1) return __ldcs(p);
@@ -192,7 +197,7 @@ __device__ __forceinline__ void pdl_enter() {
 // a fixed shuffle tree (and, for T > 32, a fixed smem combine of the warp sums).
 constexpr int CSR_U = 4;
 
-template <int T, int STREAM>
+template <int T, int STREAM, bool I16>
 __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* __restrict__ x, double* y,
                                                  const double* aux, double omega, const double* dotw, Red red,
                                                  const int* done) {
@@ -209,6 +214,7 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
         double s = 0.0;
         if (row < M.n_rows) {
             const int b = __ldg(M.rp + row), e = __ldg(M.rp + row + 1);
+            const double* xr = I16 ? x + __ldg(M.cb + row) : x;
             for (int k0 = b + t; k0 < e; k0 += T * CSR_U) {
                 double v[CSR_U], xv[CSR_U];
                 int c[CSR_U];
@@ -219,11 +225,12 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
                     c[u] = 0;
                     if (k < e) {
                         v[u] = ld_mat<STREAM>(M.v + k);
-                        c[u] = ld_mat<STREAM>(M.ci + k);
+                        if constexpr (I16) c[u] = ld_mat<STREAM>(M.ci16 + k);
+                        else c[u] = ld_mat<STREAM>(M.ci + k);
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < CSR_U; ++u) xv[u] = (k0 + u * T < e) ? __ldg(x + c[u]) : 0.0;
+                for (int u = 0; u < CSR_U; ++u) xv[u] = (k0 + u * T < e) ? __ldg(xr + c[u]) : 0.0;
 #pragma unroll
                 for (int u = 0; u < CSR_U; ++u) s = fma(v[u], xv[u], s);
             }
@@ -349,7 +356,7 @@ __global__ void __launch_bounds__(kBlock) k_sbsr3(DSbsr3 M, int epi, const doubl
 // each group costs ONE memory round trip — values and x gathers are issued
 // together because the x addresses are already known.
 struct SellChunk {
-    int len, row, w;
+    int len, row, w, cb;
     long long base;
     double av, dw;
     bool act;
@@ -369,12 +376,19 @@ __device__ __forceinline__ SellChunk sell_chunk(const DSell& M, int ch, int lane
     const int2 mw = __ldg(M.meta + sub);
     c.w = M.chh == 32 ? mw.y : (int)__reduce_max_sync(0xffffffffu, (unsigned)mw.y);
     c.base = (long long)mw.x * M.chh + (srow % M.chh);
+    c.cb = (c.act && M.ci16) ? __ldg(M.cb + srow) : 0;
     c.av = (c.act && need_aux) ? aux[c.row] : 0.0;
     c.dw = (c.act && dotw) ? dotw[c.row] : 0.0;
     return c;
 }
 
-template <int U, int STREAM, int MINB>
+template <int STREAM, bool I16>
+__device__ __forceinline__ int sell_col(const DSell& M, long long idx) {
+    if constexpr (I16) return ld_mat<STREAM>(M.ci16 + idx);
+    else return ld_mat<STREAM>(M.ci + idx);
+}
+
+template <int U, int STREAM, int MINB, bool I16>
 __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const double* __restrict__ x, double* y,
                                                   const double* aux, double omega, const double* dotw, Red red,
                                                   const int* done) {
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const d
     if (ch < M.nchunks) {
         nx = sell_chunk<STREAM>(M, ch, lane, need_aux, aux, dotw);
 #pragma unroll
-        for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? ld_mat<STREAM>(M.ci + nx.base + SS * u) : 0;
+        for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? sell_col<STREAM, I16>(M, nx.base + SS * u) : 0;
     }
     while (ch < M.nchunks) {
         const SellChunk cu = nx;
@@ -409,15 +423,15 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const d
                 cc[u] = cn[u];
                 const bool p = j0 + u < cu.len;
                 v[u] = p ? ld_mat<STREAM>(M.v + cu.base + SS * (j0 + u)) : 0.0;
-                xv[u] = p ? __ldg(x + cc[u]) : 0.0;
+                xv[u] = p ? __ldg(x + cu.cb + cc[u]) : 0.0;
             }
             if (j0 + U < cu.w) {
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    cn[u] = (j0 + U + u < cu.len) ? ld_mat<STREAM>(M.ci + cu.base + SS * (j0 + U + u)) : 0;
+                    cn[u] = (j0 + U + u < cu.len) ? sell_col<STREAM, I16>(M, cu.base + SS * (j0 + U + u)) : 0;
             } else if (chn < M.nchunks) {
 #pragma unroll
-                for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? ld_mat<STREAM>(M.ci + nx.base + SS * u) : 0;
+                for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? sell_col<STREAM, I16>(M, nx.base + SS * u) : 0;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u)
@@ -662,7 +676,7 @@ __device__ void tail_csr(const TailOp& op, double* wsum) {
                 for (int u = 0; u < CSR_U; ++u) {
                     const int kk = k0 + u * T;
                     v[u] = kk < e ? __ldg(M.v + kk) : 0.0;
-                    c[u] = kk < e ? __ldg(M.ci + kk) : 0;
+                    c[u] = kk < e ? (M.ci16 ? __ldg(M.cb + row) + (int)__ldg(M.ci16 + kk) : __ldg(M.ci + kk)) : 0;
                 }
 #pragma unroll
                 for (int u = 0; u < CSR_U; ++u) xv[u] = (k0 + u * T < e) ? __ldcg(op.x + c[u]) : 0.0;
@@ -876,6 +890,10 @@ int occ_grid(K kern, long long work_units_per_cta_needed, size_t smem = 0) {
 }  // namespace
 
 // ------------------------------------------------------------------ host API
+// Kernel pointer for an operand's index width (same signature either way).
+#define SELLK(UU, P, MB) (M.sell.ci16 ? k_sell<UU, P, MB, true> : k_sell<UU, P, MB, false>)
+#define CSRK(GG, P) (M.csr.ci16 ? k_csr<GG, P, true> : k_csr<GG, P, false>)
+
 int spmv_grid(const DMat& M) {
     if (M.fmt == 1) {
         const long long ch = (M.sb.nchunks + 7) / 8;
@@ -901,8 +919,8 @@ int spmv_grid(const DMat& M) {
         const int st = M.sell.pol;
 #define ASPAMG_SELL_OCC(UU, MB)                                                                  \
     if (M.sell.u == UU * 10 + MB)                                                                \
-        return st == 1 ? occ_grid(k_sell<UU, 1, MB>, ch)                                         \
-                       : st == 2 ? occ_grid(k_sell<UU, 2, MB>, ch) : occ_grid(k_sell<UU, 0, MB>, ch);
+        return st == 1 ? occ_grid(SELLK(UU, 1, MB), ch)                                          \
+                       : st == 2 ? occ_grid(SELLK(UU, 2, MB), ch) : occ_grid(SELLK(UU, 0, MB), ch);
         ASPAMG_SELL_OCC(8, 1)
         ASPAMG_SELL_OCC(8, 3)
         ASPAMG_SELL_OCC(8, 4)
@@ -917,7 +935,7 @@ int spmv_grid(const DMat& M) {
     const long long ctas = ((long long)M.csr.n_rows * T + kBlock - 1) / kBlock;
     const int st = M.csr.pol;
 #define ASPAMG_CSR_OCC(TT) \
-    case TT: return st == 1 ? occ_grid(k_csr<TT, 1>, ctas) : st == 2 ? occ_grid(k_csr<TT, 2>, ctas) : occ_grid(k_csr<TT, 0>, ctas);
+    case TT: return st == 1 ? occ_grid(CSRK(TT, 1), ctas) : st == 2 ? occ_grid(CSRK(TT, 2), ctas) : occ_grid(CSRK(TT, 0), ctas);
     switch (T) {
         ASPAMG_CSR_OCC(1)
         ASPAMG_CSR_OCC(2)
@@ -968,11 +986,11 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
 #define ASPAMG_SELL(UU, MB)                                                                                          \
     if (M.sell.u == UU * 10 + MB) {                                                                                 \
         if (M.sell.pol == 1)                                                                                        \
-            launch(k_sell<UU, 1, MB>, grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);     \
+            launch(SELLK(UU, 1, MB), grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);      \
         else if (M.sell.pol == 2)                                                                                   \
-            launch(k_sell<UU, 2, MB>, grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);     \
+            launch(SELLK(UU, 2, MB), grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);      \
         else                                                                                                        \
-            launch(k_sell<UU, 0, MB>, grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);     \
+            launch(SELLK(UU, 0, MB), grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);      \
         return;                                                                                                     \
     }
         ASPAMG_SELL(8, 1)
@@ -988,11 +1006,11 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
 #define ASPAMG_CSR_CASE(GG)                                                                                   \
     case GG:                                                                                                  \
         if (M.csr.pol == 1)                                                                                   \
-            launch(k_csr<GG, 1>, grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
+            launch(CSRK(GG, 1), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);       \
         else if (M.csr.pol == 2)                                                                              \
-            launch(k_csr<GG, 2>, grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
+            launch(CSRK(GG, 2), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);       \
         else                                                                                                  \
-            launch(k_csr<GG, 0>, grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
+            launch(CSRK(GG, 0), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);       \
         break;
     switch (M.csr.group) {
         ASPAMG_CSR_CASE(1)

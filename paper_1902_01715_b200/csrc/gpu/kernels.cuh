@@ -23,6 +23,10 @@ struct DCsr {
     double* v = nullptr;
     int group = 1;
     int pol = 0;  // L2 policy of the matrix stream: 0 default, 1 evict-first, 2 evict-last
+    // 16-bit column offsets (instead of ci) when every row's columns span < 2^16:
+    // column = cb[row] + ci16[k] (10 instead of 12 matrix bytes per entry)
+    unsigned short* ci16 = nullptr;
+    int* cb = nullptr;
 };
 
 // Sliced 3x3-block format for an exactly 3x3-blocked operator (K): block
@@ -60,6 +64,8 @@ struct DSell {
     int* ci = nullptr;
     double* v = nullptr;
     int pol = 0;
+    unsigned short* ci16 = nullptr;  // 16-bit column offsets: column = cb[slot row] + ci16[slot]
+    int* cb = nullptr;
 };
 
 // One matrix operand.

@@ -274,7 +274,7 @@ def test_coarse_tail_persistent_kernel_matches_oracle(pkg, oracle, tail_rows):
 
 @pytest.mark.parametrize("opts", [{"sell_chh": 8}, {"sell_chh": 32, "sell_sort_fill_pct": 100000},
                                   {"sell_sort": 1}, {"sell_sort": 1, "sell_sigma": 256}, {"sell_u": 41}, {"sell_u": 21},
-                                  {"sell_tma": 164}, {"sell_tma": 82}, {"pdl": 0}])
+                                  {"sell_tma": 164}, {"sell_tma": 82}, {"pdl": 0}, {"idx16": 0}, {"idx16": 0, "sell_chh": 8}])
 def test_sell_layout_variants_are_bit_identical(pkg, opts):
     """Every SELL layout/kernel variant sums each row sequentially in ascending
     column order, so the V-cycle output is bit-identical across variants."""
