@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -96,7 +97,7 @@ void slice_meta(const std::vector<int>& len, std::vector<int2>& meta, long long&
     for (int ch = 0; ch < nch; ++ch) {
         int w = 0;
         for (int l = 0; l < h && ch * h + l < n; ++l) w = std::max(w, len[(size_t)ch * h + l]);
-        if (slots > (1ll << 31) / 288) throw Fail{4, "sliced layout exceeds int32 slot indexing"};
+        if (slots > INT_MAX - 65536) throw Fail{4, "sliced layout exceeds int32 slot offsets"};
         meta[(size_t)ch] = make_int2((int)slots, w);
         slots += w;
     }
