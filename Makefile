@@ -13,8 +13,9 @@ GPUHDR   := $(wildcard $(PKG)/csrc/gpu/*.cuh) include/aspamg_gpu.h
 NVCC     := /usr/local/cuda/bin/nvcc
 # /usr/bin/g++ explicitly: the image exports CXX=/opt/gcc/bin/g++, which lacks libgomp
 CXX      := /usr/bin/g++
-# Portable x86-64 baseline: the GPU box's host CPU is not this container's.
-CXXFLAGS := -std=c++20 -O3 -march=x86-64-v2 -ffp-contract=off -fPIC -fopenmp -Wall -Wextra
+# x86-64-v3 (AVX2) baseline: the GPU box's host CPU is not this container's (both have AVX2/AVX-512);
+# -ffp-contract=off keeps every sum in source order, so results do not depend on the vector width.
+CXXFLAGS := -std=c++20 -O3 -march=x86-64-v3 -ffp-contract=off -fPIC -fopenmp -Wall -Wextra
 NVFLAGS  := -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a \
             -ccbin /usr/bin/g++ -Xcompiler -fPIC -Xcompiler -fopenmp -Xcompiler -ffp-contract=off -Xptxas -v --expt-relaxed-constexpr
 

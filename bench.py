@@ -101,8 +101,10 @@ def file_hash(path):
     return h.hexdigest()[:12]
 
 
-def get_hierarchy(P, cfg, scale, rank, dist, threads):
-    """CPU setup once (rank 0), cached on disk for the other ranks / reruns."""
+def get_hierarchy(P, cfg, scale, rank, dist, threads, setup_device=None):
+    """Setup once (rank 0), cached on disk for the other ranks / reruns. With
+    setup_device the SRQCG and Galerkin phases run on that GPU (bit-identical
+    hierarchy, tests/test_gpu_setup.py)."""
     from paper_1902_01715_b200 import _native as N
     t0 = time.perf_counter()
     prob = P.Problem.config(cfg, scale)
@@ -114,7 +116,7 @@ def get_hierarchy(P, cfg, scale, rank, dist, threads):
     t_setup = None
     if rank == 0 and not os.path.exists(path):
         t0 = time.perf_counter()
-        h = P.Hierarchy.setup(prob.K, prob.coords, threads=threads)
+        h = P.Hierarchy.setup(prob.K, prob.coords, threads=threads, setup_device=setup_device)
         t_setup = time.perf_counter() - t0
         h.save(path + ".tmp")
         os.replace(path + ".tmp", path)

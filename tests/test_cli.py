@@ -65,7 +65,7 @@ def test_cli_matrix_market_input(tmp_path, pkg):
         f.write("%%MatrixMarket matrix coordinate real symmetric\n% generated\n")
         f.write(f"{K.shape[0]} {K.shape[1]} {int(low.sum())}\n")
         for i, j, v in zip(K.row[low], K.col[low], K.data[low]):
-            f.write(f"{i + 1} {j + 1} {v!r}\n")
+            f.write(f"{i + 1} {j + 1} {float(v)!r}\n")
     xyz = tmp_path / "xyz.txt"
     np.savetxt(xyz, p.coords)
     r = run("--matrix", str(mtx), "--coords", str(xyz))

@@ -287,5 +287,5 @@ def test_sell_layout_variants_are_bit_identical(pkg, opts):
     g = _gpu(pkg, h, **opts)
     assert np.array_equal(g.apply(y), ref)
     if "pdl" in opts:
-        g2 = _gpu(pkg, h, pdl=1)  # restore the process-wide default
+        g2 = _gpu(pkg, h, pdl=1, sell_chh=32, sell_sort_fill_pct=100000, sell_min_mean=1)  # restore the default
         assert np.array_equal(g2.apply(y), ref)

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--scale", type=int, default=1)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "full_configs.json"))
     ap.add_argument("--oracle", type=int, default=1, help="run the CPU oracle solve (0 = GPU only)")
+    ap.add_argument("--gpu-setup", type=int, default=0, help="SRQCG + Galerkin on the GPU (bit-identical hierarchy)")
     args = ap.parse_args()
 
     class D:
@@ -43,9 +44,14 @@ def main():
     threads = os.cpu_count() or 1
     for cfg in args.configs:
         t0 = time.perf_counter()
-        prob, h, t_gen, t_setup = bench.get_hierarchy(P, cfg, args.scale, 0, D(), threads)
+        prob, h, t_gen, t_setup = bench.get_hierarchy(P, cfg, args.scale, 0, D(), threads,
+                                                      0 if args.gpu_setup else None)
         info = h.info()
+        print(cfg, "setup", round(t_gen, 1), round(t_setup, 1), {k: round(getattr(info, k), 2) for k in
+              ("T_ts", "T_sm", "T_cs", "T_pl", "T_rap")}, flush=True)
         rec = {"config": bench.CONFIG_DESC[cfg], "n": prob.K.n_rows, "nnz": prob.K.nnz, "setup_s": t_setup,
+               "gen_s": t_gen, "gpu_setup": bool(args.gpu_setup),
+               "setup_phases": {k: getattr(info, k) for k in ("T_ts", "T_sm", "T_cs", "T_pl", "T_rap")},
                "levels": int(info.n_levels), "C_gd": info.C_gd, "C_op": info.C_op, "C_fs": info.C_fs,
                "level_sizes": [int(h.level_view(l).A.n_rows) for l in range(info.n_levels)]}
         g = P.GpuVcycle(h)

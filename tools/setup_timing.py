@@ -38,7 +38,8 @@ def main():
     res = []
     for cfg in [int(c) for c in a.configs.split(",")]:
         p = P.Problem.config(cfg, a.scale)
-        P.amg_setup(P.Problem.config(1, 4).K, None, setup_device=0)  # context / module warm-up
+        warm = P.Problem.config(1, 4)
+        P.amg_setup(warm.K, warm.coords, setup_device=0)  # CUDA context / module warm-up
         t = time.perf_counter()
         hc = P.amg_setup(p.K, p.coords)
         tc = time.perf_counter() - t
