@@ -249,7 +249,10 @@ def run_b200(args, ws, rank, local):
     from paper_1902_01715_b200 import _native as N
     dist = Dist(ws, rank, local, "nccl")
     threads = max(1, (os.cpu_count() or 1) // max(1, ws))
-    prob, h, t_gen, t_setup = get_hierarchy(P, args.config, args.scale, rank, dist, os.cpu_count() or 1)
+    # setup (outside the timed region): CPU, with the SRQCG + Galerkin phases on this
+    # rank's GPU — the identical hierarchy the all-CPU setup builds (tests/test_gpu_setup.py)
+    prob, h, t_gen, t_setup = get_hierarchy(P, args.config, args.scale, rank, dist, os.cpu_count() or 1,
+                                            None if args.cpu_setup else local)
     info = h.info()
     t0 = time.perf_counter()
     g = P.GpuVcycle(h, device=local)
@@ -388,7 +391,8 @@ def run_b200(args, ws, rank, local):
                    "levels": int(info.n_levels), "C_gd": info.C_gd, "C_op": info.C_op, "C_fs": info.C_fs,
                    "n_it": n_iters, "converged": converged, "true_rel_res": per_solve[-1][3],
                    "rel_tol": args.tol, "K_format": "bsr3" if lv0.a_format == 1 else "csr",
-                   "setup_s": t_setup, "upload_s": t_upload, "parallelism": f"replicas x{ws}",
+                   "setup_s": t_setup, "setup_on": "cpu" if args.cpu_setup else "cpu + gpu (srqcg, galerkin)",
+                   "upload_s": t_upload, "parallelism": f"replicas x{ws}",
                    "l2": "inputs larger than L2 (K alone > 126 MB), no flush" if args.config != 1 else "K fits in L2"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": top[0], "level": top[1], "kernel_ms": k_ms,
@@ -426,6 +430,8 @@ def main():
     ap.add_argument("--ref-sample-s", dest="ref_sample_s", type=float, default=12.0)
     ap.add_argument("--full-iters", dest="full_iters", type=int, default=0)
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
+    ap.add_argument("--cpu-setup", dest="cpu_setup", action="store_true",
+                    help="run the whole setup on the CPU (default: SRQCG + Galerkin on the GPU, same hierarchy)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = dist_env()

@@ -265,7 +265,11 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     A.n_rows = (int)v.n_rows;
     A.n_cols = (int)v.n_cols;
     A.nnz = nnz;
-    const bool i16 = c->opt_idx16 && rows_fit_u16(v);
+    A.group = group_for(mean, maxlen, v.n_rows, (double)c->opt_csr_per_thread);
+    // 16-bit offsets pay off for short rows (few threads per row, index bytes a
+    // larger share of the per-thread stream); long-row operands (group >= 32)
+    // measured slower with them (tools/tune_kernels.py, profiles/README.md)
+    const bool i16 = c->opt_idx16 && A.group <= c->opt_idx16_max_group && rows_fit_u16(v);
     std::vector<int> rp((size_t)v.n_rows + 1), ci(i16 ? 0 : (size_t)nnz), cb(i16 ? (size_t)std::max<int64_t>(v.n_rows, 1) : 0);
     std::vector<unsigned short> c16(i16 ? (size_t)nnz : 0);
     for (int64_t i = 0; i <= v.n_rows; ++i) rp[(size_t)i] = (int)(v.n_rows ? v.row_offsets[i] : 0);
@@ -294,7 +298,6 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         if (nnz) CK(cudaMemcpy(A.ci, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
     if (nnz) CK(cudaMemcpy(A.v, v.values, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice));
-    A.group = group_for(mean, maxlen, v.n_rows, (double)c->opt_csr_per_thread);
     A.pol = (long long)(12.0 * nnz) > c->opt_stream_bytes ? 1 : 0;
     return M;
 }
@@ -763,6 +766,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "tail_rows") c->opt_tail_rows = value;
         else if (k == "csr_per_thread") c->opt_csr_per_thread = std::max<int64_t>(1, value);
         else if (k == "idx16") c->opt_idx16 = value;
+        else if (k == "idx16_max_group") c->opt_idx16_max_group = value;
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;
         else if (k == "sell_max_len") c->opt_sell_max_len = value;
         else if (k == "sell_min_rows") c->opt_sell_min_rows = value;

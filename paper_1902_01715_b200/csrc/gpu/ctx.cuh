@@ -65,6 +65,7 @@ struct aspamg_gpu_ctx {
               opt_sell_u = 0, opt_sell_tma = 0, opt_sell_chh = 0, opt_sell_sort = 0,
               opt_sell_min_mean = 8;
     long long opt_idx16 = 1;  // 16-bit column offsets where every row spans < 2^16 columns
+    long long opt_idx16_max_group = 16;  // ... and (CSR) at most this many threads per row
     long long opt_stream_bytes = 48ll << 20, opt_keep_bytes = 64ll << 20, opt_tail_rows = 0, opt_csr_per_thread = 4;
     // PCG state and vectors
     PcgState* st = nullptr;       // device
