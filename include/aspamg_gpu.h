@@ -112,6 +112,19 @@ int aspamg_gpu_srqcg(void* device, const aspamg_csr_view* A, const aspamg_csr_vi
 int aspamg_gpu_galerkin(void* device, const aspamg_csr_view* P, const aspamg_csr_view* Pt,
                         const aspamg_csr_view* A, aspamg_csr_alloc_fn alloc, void* sink);
 
+/* GPU setup: adaptive FSAI smoother set-up (aFSAI build,
+ * Lanczos lambda_max x 1.05, omega = min(1, 2/lambda), refinement passes; fsai.hpp:27-83,
+ * SPEC.md:157-232) with the host's operation order — bit-identical G, omega, lambda.
+ * G is written through alloc(sink, ...); psi[n] receives the final pass's Schur
+ * complements; exit_reason 0 omega reached, 1 density bound, 2 pattern stagnation.
+ * Signature = aspamg_smoother_fn of aspamg_host.h. device = (void*)(intptr_t)index. */
+int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A, const aspamg_smoother_params* prm,
+                              aspamg_csr_alloc_fn alloc, void* sink, double* psi, double* omega,
+                              double* lambda_hat, int64_t* passes, int* exit_reason);
+/* aFSAI build alone from the identity start, for verification. */
+int aspamg_gpu_afsai_build(void* device, const aspamg_csr_view* A, int64_t k, int64_t rho, double eps,
+                           aspamg_csr_alloc_fn alloc, void* sink, double* psi);
+
 /* measurement helpers */
 int aspamg_gpu_last_solve_ms(aspamg_gpu_ctx* ctx, double* ms);      /* device time of the last pcg */
 int aspamg_gpu_launch_count(aspamg_gpu_ctx* ctx, int64_t* n);       /* kernels launched by the last pcg */

@@ -109,6 +109,13 @@ int aspamg_set_galerkin_backend(aspamg_galerkin_fn fn, void* user);
  * is owned by *out (free with aspamg_csr_free). */
 int aspamg_galerkin(const aspamg_csr_view* P, const aspamg_csr_view* A, aspamg_csr_owned** out,
                     aspamg_csr_view* out_view);
+/* Smoother backend: when set, aspamg_setup runs every level's
+ * adaptive FSAI set-up through fn (e.g. aspamg_gpu_smoother_setup); the host forms the
+ * Kaporin estimate from the returned psi. NULL restores the CPU path. Process-wide. */
+typedef int (*aspamg_smoother_fn)(void* user, const aspamg_csr_view* A, const aspamg_smoother_params* prm,
+                                  aspamg_csr_alloc_fn alloc, void* sink, double* psi, double* omega,
+                                  double* lambda_hat, int64_t* passes, int* exit_reason);
+int aspamg_set_smoother_backend(aspamg_smoother_fn fn, void* user);
 /* aFSAI build from the identity start: returns G via a new hierarchy-owned
  * buffer set; G_out views stay valid until aspamg_csr_free. */
 int aspamg_afsai_build(const aspamg_csr_view* A, int64_t k, int64_t rho, double eps, aspamg_csr_owned** G,

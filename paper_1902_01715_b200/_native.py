@@ -26,6 +26,13 @@ class CsrView(C.Structure):
                 ("row_offsets", P_i64), ("col_indices", P_i64), ("values", P_dbl)]
 
 
+class SmootherParams(C.Structure):
+    """aspamg_smoother_params (include/aspamg_csr.h)."""
+    _fields_ = [("k0", C.c_int64), ("rho0", C.c_int64), ("eps0", C.c_double), ("ki", C.c_int64),
+                ("rhoi", C.c_int64), ("epsi", C.c_double), ("omega_bar", C.c_double), ("rho_bar", C.c_double),
+                ("lanczos_steps", C.c_int64), ("seed", C.c_uint64)]
+
+
 class SetupConfig(C.Structure):
     _fields_ = [("k0", i64), ("rho0", i64), ("eps0", dbl),
                 ("ki", i64), ("rhoi", i64), ("epsi", dbl),
@@ -105,6 +112,7 @@ def host() -> C.CDLL:
         lib.aspamg_csr_free.restype = None
         lib.aspamg_set_srqcg_backend.argtypes = [C.c_void_p, C.c_void_p]
         lib.aspamg_set_galerkin_backend.argtypes = [C.c_void_p, C.c_void_p]
+        lib.aspamg_set_smoother_backend.argtypes = [C.c_void_p, C.c_void_p]
         lib.aspamg_galerkin.argtypes = [C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(C.c_void_p),
                                         C.POINTER(CsrView)]
         _host = lib
@@ -155,6 +163,9 @@ def gpu() -> C.CDLL:
         lib.aspamg_gpu_srqcg.argtypes = [vp, C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(CsrView), P_dbl, i64, i64,
                                          i64, dbl, C.c_uint64, P_dbl, P_dbl, P_i64, P_i64, C.POINTER(C.c_int)]
         lib.aspamg_gpu_galerkin.argtypes = [vp, C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(CsrView), vp, vp]
+        lib.aspamg_gpu_afsai_build.argtypes = [vp, C.POINTER(CsrView), i64, i64, dbl, vp, vp, P_dbl]
+        lib.aspamg_gpu_smoother_setup.argtypes = [vp, C.POINTER(CsrView), C.POINTER(SmootherParams), vp, vp, P_dbl,
+                                                  P_dbl, P_dbl, P_i64, C.POINTER(C.c_int)]
         _gpu = lib
     return _gpu
 

@@ -139,6 +139,15 @@ inline T* dalloc(aspamg_gpu_ctx* c, size_t count) {
     return static_cast<T*>(p);
 }
 
+// Free one dalloc'ed block before the context ends (setup scratch).
+inline void dfree(aspamg_gpu_ctx* c, void* p) {
+    if (!p) return;
+    auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
+    if (it == c->allocs.end()) return;
+    cudaFree(p);
+    c->allocs.erase(it);
+}
+
 inline Red make_red(aspamg_gpu_ctx* c, int grid, int fin, double* out = nullptr) {
     Site s;
     s.partials = dalloc<double>(c, 2 * (size_t)std::max(grid, 1));

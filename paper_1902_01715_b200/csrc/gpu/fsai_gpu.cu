@@ -1,0 +1,712 @@
+// GPU setup components: the adaptive FSAI smoother
+// set-up — aFSAI build, Lanczos lambda_max, the omega refinement loop
+// (Alg. 3 :374-387) — on the device.
+//
+// Restates csrc/host/fsai.cpp operation for operation, so G, omega and psi are
+// bit-identical to the host's:
+//   * afsai_build: one warp per row; the row's incremental Cholesky factor of
+//     A[P, P] (packed lower triangle), bordered solves and the gradient
+//     accumulator (open-addressing table keyed by column) live in shared
+//     memory. Every sum keeps the host order: dot4's four partial chains run on
+//     lanes 0..3 and combine as (s0 + s1) + (s2 + s3); the transposed solve's
+//     subtraction chain runs on lane 0 over products formed by all lanes; the
+//     gradient takes the pattern rows in insertion order, then row i. Candidate
+//     choice = the host's partial_sort order (|g| descending, column ascending).
+//   * transpose: counting sort by column + per-column sort by row (the unique
+//     transpose, identical to core.cpp transpose()).
+//   * Lanczos: exact sequential CSR products (thread per row, ascending column
+//     order) and core.cpp's chunked dots; the tridiagonal eigenproblem and the
+//     start vector (Rng) on the host, same code.
+#include "setup_common.cuh"
+#include "../host/core.hpp"
+#include "../host/smalldense.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace aspamg_gpu {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+struct AfsaiArgs {
+    DCsr64 A;
+    const long long* gs_rp = nullptr;  // start pattern (G of the previous pass) or null
+    const long long* gs_ci = nullptr;
+    int k = 0, rho = 0;
+    double eps = 0.0;
+    int mcap = 1, hcap = 1024;
+    int l_global = 0;            // factor in global scratch (rows too long for shared memory)
+    double* lscratch = nullptr;  // [gridDim.x * W][LP] when l_global
+    const long long* rows = nullptr;  // rows to process (null: all)
+    long long nrows = 0;
+    int* cnt = nullptr;          // per row: m + 1 entries; -1 not SPD; -2 table overflow
+    long long* ocol = nullptr;   // n x (mcap + 1) scratch, row sorted by column
+    double* oval = nullptr;
+    double* psi = nullptr;
+    unsigned long long* bad = nullptr;  // smallest failing row
+};
+
+__host__ __device__ inline size_t packed(long long m) { return (size_t)m * (size_t)(m + 1) / 2; }
+
+__host__ __device__ inline size_t warp_bytes(int mcap, int hcap, bool l_global) {
+    const size_t lp = l_global ? 0 : packed(mcap);
+    size_t b = 8 * (lp + 3 * (size_t)mcap + (size_t)hcap) + 4 * ((size_t)hcap + (size_t)mcap + 40);
+    return (b + 15) & ~(size_t)15;
+}
+
+struct WarpMem {
+    double *L, *y, *a, *pr, *hv;
+    int *hk, *pat, *sel;
+};
+
+__device__ __forceinline__ unsigned hslot(int j, int cap) { return ((unsigned)j * 2654435761u) & (unsigned)(cap - 1); }
+
+// A(r, c) of a sorted-row CSR, 0 if not stored (the host's dense scatter).
+__device__ double a_at(const DCsr64& A, long long r, long long c) {
+    long long lo = A.rp[r], hi = A.rp[r + 1];
+    const long long end = hi;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (A.ci[mid] < c) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < end && A.ci[lo] == c) ? A.v[lo] : 0.0;
+}
+
+// smalldense.cpp dot4 with its four partial chains on lanes 0..3; result on every lane.
+__device__ double dot4w(const double* x, const double* y, int n, int lane) {
+    double s = 0.0;
+    const int n4 = n & ~3;
+    if (lane < 4) {
+        for (int k = lane; k < n4; k += 4) s = __dadd_rn(s, __dmul_rn(x[k], y[k]));
+        if (lane == 0)
+            for (int k = n4; k < n; ++k) s = __dadd_rn(s, __dmul_rn(x[k], y[k]));
+    }
+    const double s1 = __shfl_sync(FULL, s, 1), s2 = __shfl_sync(FULL, s, 2), s3 = __shfl_sync(FULL, s, 3);
+    const double r = __dadd_rn(__dadd_rn(s, s1), __dadd_rn(s2, s3));
+    return __shfl_sync(FULL, r, 0);
+}
+
+// smalldense.cpp trsv_lower on the packed factor (b may be the factor's row n).
+__device__ void trsv_lower_w(int n, const double* L, double* b, int lane) {
+    for (int i = 0; i < n; ++i) {
+        const double* Li = L + packed(i);
+        const double d = dot4w(Li, b, i, lane);
+        if (lane == 0) b[i] = __ddiv_rn(__dsub_rn(b[i], d), Li[i]);
+        __syncwarp();
+    }
+}
+
+// smalldense.cpp trsv_lower_t: s = b_i - L_{i+1,i} b_{i+1} - ... (sequential), products by all lanes.
+__device__ void trsv_lower_t_w(int n, const double* L, double* b, double* pr, int lane) {
+    for (int i = n - 1; i >= 0; --i) {
+        for (int k = i + 1 + lane; k < n; k += 32) pr[k] = __dmul_rn(L[packed(k) + i], b[k]);
+        __syncwarp();
+        if (lane == 0) {
+            double s = b[i];
+            for (int k = i + 1; k < n; ++k) s = __dsub_rn(s, pr[k]);
+            b[i] = __ddiv_rn(s, L[packed(i) + i]);
+        }
+        __syncwarp();
+    }
+}
+
+// fsai.cpp chol_append: row m of the factor from A[j, pat[0..m)].
+__device__ bool chol_append_w(const DCsr64& A, const WarpMem& w, int m, long long j, int lane) {
+    double* row = w.L + packed(m);
+    for (int q = lane; q < m; q += 32) row[q] = a_at(A, j, w.pat[q]);
+    double ajj = lane == 0 ? a_at(A, j, j) : 0.0;
+    ajj = __shfl_sync(FULL, ajj, 0);
+    __syncwarp();
+    trsv_lower_w(m, w.L, row, lane);
+    const double d = __dsub_rn(ajj, dot4w(row, row, m, lane));
+    if (!(d > 0.0)) return false;
+    if (lane == 0) row[m] = __dsqrt_rn(d);
+    __syncwarp();
+    return true;
+}
+
+__device__ int h_insert(int* hk, double* hv, int hcap, int key, bool& ovf) {
+    unsigned h = hslot(key, hcap);
+    for (int p = 0; p < hcap; ++p) {
+        const int k = hk[h];
+        if (k == key) return (int)h;
+        if (k == -1) {
+            const int old = atomicCAS(&hk[h], -1, key);
+            if (old == -1) {
+                hv[h] = 0.0;  // first touch: grad[j] = 0.0
+                return (int)h;
+            }
+            if (old == key) return (int)h;
+        }
+        h = (h + 1) & (unsigned)(hcap - 1);
+    }
+    ovf = true;
+    return -1;
+}
+
+__device__ int h_find(const int* hk, int hcap, int key) {
+    unsigned h = hslot(key, hcap);
+    for (int p = 0; p < hcap; ++p) {
+        const int k = hk[h];
+        if (k == key) return (int)h;
+        if (k == -1) return -1;
+        h = (h + 1) & (unsigned)(hcap - 1);
+    }
+    return -1;
+}
+
+// grad[j] += A(r, j) * gm for the j < i of row r (lanes take distinct j).
+__device__ void scatter_w(const DCsr64& A, long long r, double gm, long long i, const WarpMem& w, int hcap, int lane,
+                          bool& ovf) {
+    const long long b = A.rp[r], e = A.rp[r + 1];
+    for (long long q = b + lane; q < e; q += 32) {
+        const long long j = A.ci[q];
+        if (j >= i) continue;
+        const int slot = h_insert(w.hk, w.hv, hcap, (int)j, ovf);
+        if (slot >= 0) w.hv[slot] = __dadd_rn(w.hv[slot], __dmul_rn(A.v[q], gm));
+    }
+    __syncwarp();
+}
+
+// One row of afsai_build (fsai.cpp:60-160).
+__device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int lane) {
+    const DCsr64& A = P.A;
+    int m = 0;
+    bool ok = true;
+    if (P.gs_rp) {
+        const long long b = P.gs_rp[i], e = P.gs_rp[i + 1];
+        int ns = 0;
+        for (long long q = b + lane; q < e; q += 32) {
+            const long long c = P.gs_ci[q];
+            if (c < i) w.pat[q - b] = (int)c;
+        }
+        for (long long q0 = b; q0 < e; q0 += 32) {
+            const bool lt = q0 + lane < e && P.gs_ci[q0 + lane] < i;
+            ns += __popc(__ballot_sync(FULL, lt));
+        }
+        __syncwarp();
+        for (int q = 0; q < ns; ++q) {
+            if (!chol_append_w(A, w, m, w.pat[q], lane)) {
+                ok = false;
+                break;
+            }
+            ++m;
+        }
+    }
+    double aii = lane == 0 ? a_at(A, i, i) : 0.0;
+    aii = __shfl_sync(FULL, aii, 0);
+    double psi_prev = 0.0, psi = 0.0;
+    bool ovf = false;
+    for (int step = 0; ok; ++step) {
+        // bordered solve y = A_PP^{-1} a, psi = a_ii - a'y
+        for (int q = lane; q < m; q += 32) {
+            const double v = a_at(A, i, w.pat[q]);
+            w.a[q] = v;
+            w.y[q] = v;
+        }
+        __syncwarp();
+        trsv_lower_w(m, w.L, w.y, lane);
+        trsv_lower_t_w(m, w.L, w.y, w.pr, lane);
+        psi = __dsub_rn(aii, dot4w(w.a, w.y, m, lane));
+        if (!(psi > 0.0)) {
+            ok = false;
+            break;
+        }
+        if (step > 0 && __dsub_rn(psi_prev, psi) <= __dmul_rn(P.eps, psi_prev)) break;
+        if (step == P.k) break;
+        psi_prev = psi;
+        // gradient over the rows of P (insertion order) then row i
+        for (int s = lane; s < P.hcap; s += 32) w.hk[s] = -1;
+        __syncwarp();
+        for (int q = 0; q < m; ++q) scatter_w(A, w.pat[q], -w.y[q], i, w, P.hcap, lane, ovf);
+        scatter_w(A, i, 1.0, i, w, P.hcap, lane, ovf);
+        if (__any_sync(FULL, ovf)) {
+            ovf = true;
+            break;
+        }
+        for (int q = lane; q < m; q += 32) {  // exclude the pattern
+            const int sl = h_find(w.hk, P.hcap, w.pat[q]);
+            if (sl >= 0) w.hk[sl] = -2;
+        }
+        __syncwarp();
+        // the rho best candidates: |g| descending, then column ascending
+        int take = 0;
+        for (; take < P.rho; ++take) {
+            double bv = -1.0;
+            int bj = INT_MAX, bs = -1;
+            for (int s = lane; s < P.hcap; s += 32) {
+                const int key = w.hk[s];
+                if (key >= 0) {
+                    const double av = fabs(w.hv[s]);
+                    if (av > bv || (av == bv && key < bj)) {
+                        bv = av;
+                        bj = key;
+                        bs = s;
+                    }
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_down_sync(FULL, bv, o);
+                const int oj = __shfl_down_sync(FULL, bj, o), os = __shfl_down_sync(FULL, bs, o);
+                if (ov > bv || (ov == bv && oj < bj)) {
+                    bv = ov;
+                    bj = oj;
+                    bs = os;
+                }
+            }
+            bs = __shfl_sync(FULL, bs, 0);
+            bj = __shfl_sync(FULL, bj, 0);
+            if (bs < 0) break;
+            if (lane == 0) {
+                w.sel[take] = bj;
+                w.hk[bs] = -2;
+            }
+            __syncwarp();
+        }
+        if (take == 0) break;
+        if (lane == 0)  // ascending column order of the chosen candidates
+            for (int a = 1; a < take; ++a) {
+                const int v = w.sel[a];
+                int b = a - 1;
+                while (b >= 0 && w.sel[b] > v) {
+                    w.sel[b + 1] = w.sel[b];
+                    --b;
+                }
+                w.sel[b + 1] = v;
+            }
+        __syncwarp();
+        for (int c = 0; c < take && ok; ++c) {
+            const int j = w.sel[c];
+            if (lane == 0) w.pat[m] = j;
+            __syncwarp();
+            if (!chol_append_w(A, w, m, j, lane)) ok = false;
+            else ++m;
+        }
+    }
+    if (!ok) {
+        if (lane == 0) {
+            P.cnt[i] = -1;
+            atomicMin(P.bad, (unsigned long long)i);
+        }
+        return;
+    }
+    if (ovf) {
+        if (lane == 0) P.cnt[i] = -2;
+        return;
+    }
+    // row = (-y, 1) / sqrt(psi), columns ascending
+    const double s = __ddiv_rn(1.0, __dsqrt_rn(psi));
+    const long long base = i * (long long)(P.mcap + 1);
+    for (int e = lane; e <= m; e += 32) {
+        const long long col = e < m ? (long long)w.pat[e] : i;
+        const double val = e < m ? __dmul_rn(-w.y[e], s) : s;
+        int rank = 0;
+        for (int f = 0; f < m; ++f) rank += (long long)w.pat[f] < col;
+        if (e < m) rank += i < col;
+        P.ocol[base + rank] = col;
+        P.oval[base + rank] = val;
+    }
+    if (lane == 0) {
+        P.cnt[i] = m + 1;
+        P.psi[i] = psi;
+    }
+    __syncwarp();
+}
+
+__global__ void k_afsai(const AfsaiArgs P) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
+    unsigned char* p = dyn + (size_t)wid * warp_bytes(P.mcap, P.hcap, P.l_global != 0);
+    WarpMem w;
+    if (P.l_global) {
+        w.L = P.lscratch + ((size_t)blockIdx.x * W + wid) * packed(P.mcap);
+    } else {
+        w.L = reinterpret_cast<double*>(p);
+        p += 8 * packed(P.mcap);
+    }
+    w.y = reinterpret_cast<double*>(p);
+    w.a = w.y + P.mcap;
+    w.pr = w.a + P.mcap;
+    w.hv = w.pr + P.mcap;
+    w.hk = reinterpret_cast<int*>(w.hv + P.hcap);
+    w.pat = w.hk + P.hcap;
+    w.sel = w.pat + P.mcap;
+    const long long total = P.rows ? P.nrows : P.A.n_rows;
+    for (long long t = (long long)blockIdx.x * W + wid; t < total; t += (long long)gridDim.x * W)
+        afsai_row(P, w, P.rows ? P.rows[t] : t, lane);
+}
+
+// rows of the scratch -> CSR (warp per row)
+__global__ void k_compact(long long n, const long long* __restrict__ rp, int rowcap, const long long* __restrict__ ocol,
+                          const double* __restrict__ oval, long long* ci, double* v) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+        const long long b = rp[i], len = rp[i + 1] - b, src = i * (long long)rowcap;
+        for (long long q = lane; q < len; q += 32) {
+            ci[b + q] = ocol[src + q];
+            v[b + q] = oval[src + q];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- transpose
+__global__ void k_colcount(long long nnz, const long long* __restrict__ ci, int* cc) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nnz; q += (long long)gridDim.x * blockDim.x)
+        atomicAdd(&cc[ci[q]], 1);
+}
+__global__ void k_colfill(long long n, const long long* __restrict__ rp, const long long* __restrict__ ci,
+                          const double* __restrict__ v, const long long* __restrict__ trp, int* cur, long long* tci,
+                          double* tv) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+        for (long long q = rp[r]; q < rp[r + 1]; ++q) {
+            const long long c = ci[q];
+            const long long pos = trp[c] + atomicAdd(&cur[c], 1);
+            tci[pos] = r;
+            tv[pos] = v[q];
+        }
+}
+__global__ void k_segsort(long long n, const long long* __restrict__ trp, long long* tci, double* tv) {
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+        const long long b = trp[c], e = trp[c + 1];
+        for (long long a = b + 1; a < e; ++a) {
+            const long long key = tci[a];
+            const double val = tv[a];
+            long long q = a - 1;
+            while (q >= b && tci[q] > key) {
+                tci[q + 1] = tci[q];
+                tv[q + 1] = tv[q];
+                --q;
+            }
+            tci[q + 1] = key;
+            tv[q + 1] = val;
+        }
+    }
+}
+
+// y = M x, each row summed sequentially in ascending column order (spmv()).
+__global__ void k_spmv_seq(DCsr64 M, const double* __restrict__ x, double* y) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < M.n_rows;
+         r += (long long)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (long long q = M.rp[r]; q < M.rp[r + 1]; ++q) s = __dadd_rn(s, __dmul_rn(M.v[q], x[M.ci[q]]));
+        y[r] = s;
+    }
+}
+
+// w = w - (a v + b vp)   (fsai.cpp estimate_lambda_max)
+__global__ void k_lanczos_upd(long long n, double* w, const double* __restrict__ v, const double* __restrict__ vp,
+                              double a, double b) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        w[i] = __dsub_rn(w[i], __dadd_rn(__dmul_rn(a, v[i]), __dmul_rn(b, vp[i])));
+}
+
+struct DevG {  // a device CSR the setup owns, plus its host row offsets
+    DevCsr d;
+    std::vector<long long> rp;
+};
+
+void free_csr(aspamg_gpu_ctx* c, DevCsr& d) {
+    dfree(c, d.rp);
+    dfree(c, d.ci);
+    dfree(c, d.v);
+    d = DevCsr{};
+}
+
+int sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+// afsai_build on the device; A device-resident, start pattern optional.
+DevG afsai_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const DevG* Gs, int k, int rho, double eps,
+                  double* psi) {
+    cudaStream_t s = c->stream;
+    const long long n = A.n_rows;
+    long long gs_max = 0;
+    if (Gs)
+        for (long long i = 0; i < n; ++i) gs_max = std::max(gs_max, Gs->rp[(size_t)i + 1] - Gs->rp[(size_t)i]);
+    const long long mcap_ll = gs_max + (long long)k * rho + 1;
+    if (mcap_ll > 4096) throw Fail{4, "afsai (GPU): pattern bound exceeds 4096 entries per row"};
+    const int mcap = (int)mcap_ll;
+    const int rowcap = mcap + 1;
+    int* cnt = dalloc<int>(c, (size_t)std::max<long long>(n, 1));
+    long long* ocol = dalloc<long long>(c, (size_t)std::max<long long>(n, 1) * rowcap);
+    double* oval = dalloc<double>(c, (size_t)std::max<long long>(n, 1) * rowcap);
+    unsigned long long* bad = dalloc<unsigned long long>(c, 1);
+    const unsigned long long none = ~0ull;
+    CK(cudaMemcpyAsync(bad, &none, 8, cudaMemcpyHostToDevice, s));
+    const int sms = sm_count();
+    std::vector<int> hc((size_t)n);
+    std::vector<long long> todo;
+    std::vector<void*> scratch;
+    // table sizes: an upper bound of the touched columns, capped; overflowing rows rerun wider
+    const long long touch = (long long)(mcap + 1) * std::max<long long>(a_maxrow, 1);
+    int hcap = 64;
+    while (hcap < touch && hcap < 1024) hcap <<= 1;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        AfsaiArgs P;
+        P.A = A;
+        P.gs_rp = Gs ? Gs->d.rp : nullptr;
+        P.gs_ci = Gs ? Gs->d.ci : nullptr;
+        P.k = k;
+        P.rho = rho;
+        P.eps = eps;
+        P.mcap = mcap;
+        P.hcap = hcap;
+        P.cnt = cnt;
+        P.ocol = ocol;
+        P.oval = oval;
+        P.psi = psi;
+        P.bad = bad;
+        long long* drows = nullptr;
+        if (attempt > 0) {
+            drows = dalloc<long long>(c, todo.size());
+            scratch.push_back(drows);
+            CK(cudaMemcpyAsync(drows, todo.data(), todo.size() * 8, cudaMemcpyHostToDevice, s));
+            P.rows = drows;
+            P.nrows = (long long)todo.size();
+        }
+        const size_t budget = 200 * 1024;
+        bool lg = warp_bytes(mcap, hcap, false) > budget;
+        const size_t wb = warp_bytes(mcap, hcap, lg);
+        if (wb > budget) throw Fail{4, "afsai (GPU): row workspace exceeds shared memory"};
+        const int W = (int)std::max<size_t>(1, std::min<size_t>(16, budget / wb));
+        const size_t smem = wb * W;
+        CK(cudaFuncSetAttribute(k_afsai, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 1;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_afsai, 32 * W, smem));
+        const long long rows = attempt ? (long long)todo.size() : n;
+        const long long need = (rows + W - 1) / W;
+        const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)sms * std::max(occ, 1)));
+        P.l_global = lg ? 1 : 0;
+        if (lg) {
+            P.lscratch = dalloc<double>(c, (size_t)grid * W * packed(mcap));
+            scratch.push_back(P.lscratch);
+        }
+        if (rows > 0) {
+            k_afsai<<<grid, 32 * W, smem, s>>>(P);
+            CK(cudaGetLastError());
+        }
+        CK(cudaMemcpyAsync(hc.data(), cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        todo.clear();
+        for (long long i = 0; i < n; ++i)
+            if (hc[(size_t)i] == -2) todo.push_back(i);
+        if (todo.empty()) break;
+        hcap = attempt == 0 ? 4096 : 16384;
+    }
+    if (!todo.empty()) throw Fail{4, "afsai (GPU): gradient support exceeds 16384 columns in a row"};
+    unsigned long long hbad = 0;
+    CK(cudaMemcpy(&hbad, bad, 8, cudaMemcpyDeviceToHost));
+    if (hbad != none)
+        throw Fail{2, "afsai_build: non-positive local pivot at row " + std::to_string((long long)hbad)};
+    DevG G;
+    G.rp.assign((size_t)n + 1, 0);
+    for (long long i = 0; i < n; ++i) G.rp[(size_t)i + 1] = G.rp[(size_t)i] + hc[(size_t)i];
+    const long long nnz = G.rp.back();
+    G.d.rp = dalloc<long long>(c, (size_t)n + 1);
+    G.d.ci = dalloc<long long>(c, (size_t)std::max<long long>(nnz, 1));
+    G.d.v = dalloc<double>(c, (size_t)std::max<long long>(nnz, 1));
+    CK(cudaMemcpyAsync(G.d.rp, G.rp.data(), G.rp.size() * 8, cudaMemcpyHostToDevice, s));
+    k_compact<<<sms * 8, 256, 0, s>>>(n, G.d.rp, rowcap, ocol, oval, G.d.ci, G.d.v);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    for (void* q : scratch) dfree(c, q);
+    dfree(c, cnt);
+    dfree(c, ocol);
+    dfree(c, oval);
+    dfree(c, bad);
+    G.d.view = {n, n, nnz, G.d.rp, G.d.ci, G.d.v};
+    return G;
+}
+
+DevCsr transpose_device(aspamg_gpu_ctx* c, const DevG& G) {
+    cudaStream_t s = c->stream;
+    const long long n = G.d.view.n_rows, m = G.d.view.n_cols, nnz = G.d.view.nnz;
+    const int sms = sm_count();
+    int* cc = dalloc<int>(c, (size_t)std::max<long long>(m, 1));
+    CK(cudaMemsetAsync(cc, 0, (size_t)m * 4, s));
+    k_colcount<<<sms * 8, 256, 0, s>>>(nnz, G.d.ci, cc);
+    CK(cudaGetLastError());
+    std::vector<int> h((size_t)m);
+    CK(cudaMemcpyAsync(h.data(), cc, (size_t)m * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<long long> trp((size_t)m + 1, 0);
+    for (long long j = 0; j < m; ++j) trp[(size_t)j + 1] = trp[(size_t)j] + h[(size_t)j];
+    DevCsr T;
+    T.rp = dalloc<long long>(c, (size_t)m + 1);
+    T.ci = dalloc<long long>(c, (size_t)std::max<long long>(nnz, 1));
+    T.v = dalloc<double>(c, (size_t)std::max<long long>(nnz, 1));
+    CK(cudaMemcpyAsync(T.rp, trp.data(), trp.size() * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(cc, 0, (size_t)m * 4, s));
+    k_colfill<<<sms * 8, 256, 0, s>>>(n, G.d.rp, G.d.ci, G.d.v, T.rp, cc, T.ci, T.v);
+    k_segsort<<<sms * 8, 256, 0, s>>>(m, T.rp, T.ci, T.v);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));  // trp (host) outlives the copy
+    dfree(c, cc);
+    T.view = {m, n, nnz, T.rp, T.ci, T.v};
+    return T;
+}
+
+// fsai.cpp estimate_lambda_max on the device.
+double lanczos_device(DevLA& E, const DCsr64& G, const DCsr64& Gt, const DCsr64& A, long long steps,
+                      std::uint64_t seed, double* v, double* vp, double* w, double* t1, double* t2) {
+    const long long n = E.n;
+    if (n == 0) return 1.05;
+    const int sms = sm_count();
+    aspamg::Rng rng(seed);
+    std::vector<double> hv((size_t)n);
+    for (auto& x : hv) x = rng.symmetric();
+    CK(cudaMemcpyAsync(v, hv.data(), (size_t)n * 8, cudaMemcpyHostToDevice, E.s));
+    CK(cudaMemsetAsync(vp, 0, (size_t)n * 8, E.s));
+    const double nv = E.norm2(v);  // synchronises: hv outlives the copy
+    E.vec(V_DIV, v, nullptr, v, nv);
+    std::vector<double> alpha, beta;
+    double beta_prev = 0.0;
+    for (long long j = 0; j < steps; ++j) {
+        k_spmv_seq<<<sms * 8, 256, 0, E.s>>>(Gt, v, t1);
+        k_spmv_seq<<<sms * 8, 256, 0, E.s>>>(A, t1, t2);
+        k_spmv_seq<<<sms * 8, 256, 0, E.s>>>(G, t2, w);
+        CK(cudaGetLastError());
+        const double a = E.dot(w, v);
+        alpha.push_back(a);
+        k_lanczos_upd<<<E.vgrid, 256, 0, E.s>>>(n, w, v, vp, a, beta_prev);
+        CK(cudaGetLastError());
+        const double b = E.norm2(w);
+        if (j + 1 == steps || !(b > 1e-12 * std::fabs(a))) break;
+        beta.push_back(b);
+        beta_prev = b;
+        std::swap(vp, v);
+        E.vec(V_DIV, w, nullptr, v, b);
+    }
+    const int m = (int)alpha.size();
+    std::vector<double> T((size_t)m * m, 0.0), ev((size_t)m), evec((size_t)m * m);
+    for (int i = 0; i < m; ++i) {
+        T[(size_t)i * m + i] = alpha[(size_t)i];
+        if (i + 1 < m) T[(size_t)i * m + i + 1] = T[(size_t)(i + 1) * m + i] = beta[(size_t)i];
+    }
+    aspamg::sym_eig(m, T.data(), ev.data(), evec.data());
+    return 1.05 * ev[(size_t)m - 1];
+}
+
+}  // namespace
+}  // namespace aspamg_gpu
+
+using namespace aspamg_gpu;
+
+// fsai.cpp smoother_setup (Alg. 3) on the device. A: host view; G written through
+// alloc(sink, ...); psi[n] (host) receives the final pass's Schur complements
+// (the host forms the Kaporin estimate from them).
+extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A, const aspamg_smoother_params* prm,
+                                         aspamg_csr_alloc_fn alloc, void* sink, double* psi_out, double* omega,
+                                         double* lambda_hat, int64_t* passes, int* exit_reason) {
+    aspamg_gpu_ctx* c = nullptr;
+    int st = aspamg_gpu_ctx_create((int)(intptr_t)device, &c);
+    if (st != 0) return st;
+    st = guard(c, [&] {
+        if (!A || !prm || !alloc || !psi_out || !omega || !lambda_hat || !passes || !exit_reason)
+            throw Fail{4, "smoother_setup: null argument"};
+        if (A->n_rows != A->n_cols) throw Fail{1, "afsai_build: A must be square"};
+        const long long n = A->n_rows;
+        if (n > INT_MAX) throw Fail{1, "smoother_setup: n exceeds the int32 column range"};
+        long long a_maxrow = 0;
+        for (long long i = 0; i < n; ++i) a_maxrow = std::max<long long>(a_maxrow, A->row_offsets[i + 1] - A->row_offsets[i]);
+        const DevCsr dA = upload64(c, *A);
+        DevLA E;
+        E.init(c, n);
+        double* psi = dalloc<double>(c, (size_t)std::max<long long>(n, 1));
+        double* psi2 = dalloc<double>(c, (size_t)std::max<long long>(n, 1));
+        double *v = dalloc<double>(c, (size_t)n + 1), *vp = dalloc<double>(c, (size_t)n + 1),
+               *w = dalloc<double>(c, (size_t)n + 1), *t1 = dalloc<double>(c, (size_t)n + 1),
+               *t2 = dalloc<double>(c, (size_t)n + 1);
+        auto omega_of = [](double lam) {
+            if (!(lam > 0.0)) throw Fail{4, "compute_omega: lambda_hat must be positive"};
+            return std::min(1.0, 2.0 / lam);
+        };
+        DevG G = afsai_device(c, dA.view, a_maxrow, nullptr, (int)prm->k0, (int)prm->rho0, prm->eps0, psi);
+        DevCsr Gt = transpose_device(c, G);
+        double lam = lanczos_device(E, G.d.view, Gt.view, dA.view, prm->lanczos_steps, prm->seed, v, vp, w, t1, t2);
+        double om = omega_of(lam);
+        int64_t np = 0;
+        int ex = 0;  // omega_reached
+        while (om < prm->omega_bar) {
+            const double nnz_r = n ? double(G.d.view.nnz) / double(n) : 0.0;
+            if (!(nnz_r < prm->rho_bar)) { ex = 1; break; }  // density_bound
+            DevG G2 = afsai_device(c, dA.view, a_maxrow, &G, (int)prm->ki, (int)prm->rhoi, prm->epsi, psi2);
+            if (G2.d.view.nnz == G.d.view.nnz) {  // pattern_stagnation
+                free_csr(c, G2.d);
+                ex = 2;
+                break;
+            }
+            free_csr(c, G.d);
+            free_csr(c, Gt);
+            G = std::move(G2);
+            std::swap(psi, psi2);
+            Gt = transpose_device(c, G);
+            lam = lanczos_device(E, G.d.view, Gt.view, dA.view, prm->lanczos_steps, prm->seed, v, vp, w, t1, t2);
+            om = omega_of(lam);
+            ++np;
+            ex = 0;
+        }
+        int64_t *rp = nullptr, *ci = nullptr;
+        double* vals = nullptr;
+        const long long nnz = G.d.view.nnz;
+        if (alloc(sink, n, n, nnz, &rp, &ci, &vals) != 0 || !rp || (nnz && (!ci || !vals)))
+            throw Fail{5, "smoother_setup: output allocation failed"};
+        CK(cudaMemcpyAsync(rp, G.d.rp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
+        if (nnz) {
+            CK(cudaMemcpyAsync(ci, G.d.ci, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(vals, G.d.v, sizeof(double) * nnz, cudaMemcpyDeviceToHost, c->stream));
+        }
+        CK(cudaMemcpyAsync(psi_out, psi, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        *omega = om;
+        *lambda_hat = lam;
+        *passes = np;
+        *exit_reason = ex;
+    });
+    aspamg_gpu_ctx_destroy(c);
+    return st;
+}
+
+// afsai_build alone (identity start) on the device, for verification.
+extern "C" int aspamg_gpu_afsai_build(void* device, const aspamg_csr_view* A, int64_t k, int64_t rho, double eps,
+                                      aspamg_csr_alloc_fn alloc, void* sink, double* psi_out) {
+    aspamg_gpu_ctx* c = nullptr;
+    int st = aspamg_gpu_ctx_create((int)(intptr_t)device, &c);
+    if (st != 0) return st;
+    st = guard(c, [&] {
+        if (!A || !alloc) throw Fail{4, "afsai_build: null argument"};
+        if (A->n_rows != A->n_cols) throw Fail{1, "afsai_build: A must be square"};
+        const long long n = A->n_rows;
+        long long a_maxrow = 0;
+        for (long long i = 0; i < n; ++i) a_maxrow = std::max<long long>(a_maxrow, A->row_offsets[i + 1] - A->row_offsets[i]);
+        const DevCsr dA = upload64(c, *A);
+        double* psi = dalloc<double>(c, (size_t)std::max<long long>(n, 1));
+        DevG G = afsai_device(c, dA.view, a_maxrow, nullptr, (int)k, (int)rho, eps, psi);
+        int64_t *rp = nullptr, *ci = nullptr;
+        double* vals = nullptr;
+        const long long nnz = G.d.view.nnz;
+        if (alloc(sink, n, n, nnz, &rp, &ci, &vals) != 0 || !rp || (nnz && (!ci || !vals)))
+            throw Fail{5, "afsai_build: output allocation failed"};
+        CK(cudaMemcpy(rp, G.d.rp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+        if (nnz) {
+            CK(cudaMemcpy(ci, G.d.ci, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(vals, G.d.v, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+        }
+        if (psi_out) CK(cudaMemcpy(psi_out, psi, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    });
+    aspamg_gpu_ctx_destroy(c);
+    return st;
+}

@@ -14,7 +14,7 @@
 //   * the finished table is compacted and bitonic-sorted by column in shared
 //     memory and written at the row's offset (count pass + host scan + fill pass).
 // Indices stay int64 as in the reference layout (no conversion of the inputs).
-#include "ctx.cuh"
+#include "setup_common.cuh"
 
 #include <cuda_runtime.h>
 
@@ -25,13 +25,6 @@
 
 namespace aspamg_gpu {
 namespace {
-
-struct DCsr64 {
-    long long n_rows = 0, n_cols = 0, nnz = 0;
-    const long long* rp = nullptr;
-    const long long* ci = nullptr;
-    const double* v = nullptr;
-};
 
 constexpr int kWarpCap = 1024;   // table entries per warp (12 KB)
 constexpr int kWarpsPerCta = 8;  // 96 KB dynamic shared memory per CTA
@@ -195,35 +188,6 @@ __global__ void __launch_bounds__(kBigThreads) k_spgemm_big(const DCsr64 A, cons
                                                &flag, pass == 1 ? out_rp[i] : 0, out_ci, out_v);
         if (pass == 0 && threadIdx.x == 0) counts[i] = c;
     }
-}
-
-struct DevCsr {
-    long long *rp = nullptr, *ci = nullptr;
-    double* v = nullptr;
-    DCsr64 view;
-};
-
-DevCsr upload64(aspamg_gpu_ctx* c, const aspamg_csr_view& h) {
-    DevCsr d;
-    const size_t n1 = (size_t)h.n_rows + 1, nz = (size_t)h.nnz;
-    d.rp = dalloc<long long>(c, n1);
-    d.ci = dalloc<long long>(c, nz);
-    d.v = dalloc<double>(c, nz);
-    CK(cudaMemcpyAsync(d.rp, h.row_offsets, n1 * 8, cudaMemcpyHostToDevice, c->stream));
-    if (nz) {
-        CK(cudaMemcpyAsync(d.ci, h.col_indices, nz * 8, cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(d.v, h.values, nz * 8, cudaMemcpyHostToDevice, c->stream));
-    }
-    d.view = {h.n_rows, h.n_cols, h.nnz, d.rp, d.ci, d.v};
-    return d;
-}
-
-int grid_for(const void* fn, int threads, size_t smem) {
-    int dev = 0, sms = 148, occ = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
-    return sms * std::max(occ, 1);
 }
 
 // C = A B on the device (inputs device-resident); returns C device-resident.

@@ -46,6 +46,10 @@ Csr afsai_build(const Csr& A, const Csr* G_start, index_t k, index_t rho, double
 double estimate_lambda_max(const Csr& G, const Csr& Gt, const Csr& A, index_t steps, std::uint64_t seed);
 double compute_omega(double lambda_hat);
 FsaiSmoother smoother_setup(const Csr& A, const SmootherConfig& cfg);  // SPEC.md:194-202, Alg. 3
+// smoother_setup through the registered external backend (aspamg_set_smoother_backend), if any:
+// returns G, omega, lambda_hat, passes, exit reason, and psi (for the Kaporin estimate).
+bool smoother_backend_set();
+FsaiSmoother smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi);
 // x' = x + omega G'(G(b - A x)) (host reference; Gt explicit)
 std::vector<double> apply_smoothing_step(const Csr& G, const Csr& Gt, double omega, const Csr& A,
                                          const std::vector<double>& b, const std::vector<double>& x);

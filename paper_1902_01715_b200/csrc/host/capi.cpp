@@ -343,3 +343,44 @@ int aspamg_galerkin(const aspamg_csr_view* P, const aspamg_csr_view* A, aspamg_c
         *out_view = view(o->m);
     });
 }
+
+// ------------------------------------------------------ external smoother backend
+namespace {
+aspamg_smoother_fn g_smoother_fn = nullptr;
+void* g_smoother_user = nullptr;
+}  // namespace
+
+namespace aspamg {
+
+bool smoother_backend_set() { return g_smoother_fn != nullptr; }
+
+FsaiSmoother smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi) {
+    const aspamg_csr_view a = view(A);
+    aspamg_smoother_params prm{cfg.k0, cfg.rho0, cfg.eps0, cfg.ki, cfg.rhoi, cfg.epsi,
+                               cfg.omega_bar, rho_bar, cfg.lanczos_steps, cfg.seed};
+    FsaiSmoother s;
+    psi.assign(static_cast<size_t>(A.n_rows), 0.0);
+    int64_t passes = 0;
+    int exit_reason = 0;
+    const int st = g_smoother_fn(g_smoother_user, &a, &prm, csr_sink_alloc, &s.G, psi.data(), &s.omega,
+                                 &s.lambda_hat, &passes, &exit_reason);
+    if (st != 0) {
+        const std::string msg = "smoother backend failed with status " + std::to_string(st);
+        if (st == 1) throw DimensionError(msg);
+        if (st == 2) throw NotSpdError(msg);
+        if (st == 3) throw NumericalError(msg);
+        if (st == 4) throw ConfigError(msg);
+        throw std::runtime_error(msg);
+    }
+    s.refinement_passes = passes;
+    s.exit_reason = static_cast<SmootherExit>(exit_reason);
+    return s;
+}
+
+}  // namespace aspamg
+
+int aspamg_set_smoother_backend(aspamg_smoother_fn fn, void* user) {
+    g_smoother_fn = fn;
+    g_smoother_user = user;
+    return 0;
+}

@@ -233,23 +233,27 @@ FsaiSmoother smoother_setup(const Csr& A, const SmootherConfig& cfg) {
         rho_bar = A.n_rows ? 2.0 * double(lower) / double(A.n_rows) : 1.0;
     }
     std::vector<double> psi;
-    s.G = afsai_build(A, nullptr, cfg.k0, cfg.rho0, cfg.eps0, &psi);
-    Csr Gt = transpose(s.G);
-    s.lambda_hat = estimate_lambda_max(s.G, Gt, A, cfg.lanczos_steps, cfg.seed);
-    s.omega = compute_omega(s.lambda_hat);
-    s.exit_reason = SmootherExit::omega_reached;
-    while (s.omega < cfg.omega_bar) {
-        if (!(s.G.nnz_per_row() < rho_bar)) { s.exit_reason = SmootherExit::density_bound; break; }
-        std::vector<double> psi2;
-        Csr G2 = afsai_build(A, &s.G, cfg.ki, cfg.rhoi, cfg.epsi, &psi2);
-        if (G2.nnz() == s.G.nnz()) { s.exit_reason = SmootherExit::pattern_stagnation; break; }
-        s.G = std::move(G2);
-        psi.swap(psi2);
-        Gt = transpose(s.G);
+    if (smoother_backend_set()) {
+        s = smoother_external(A, cfg, rho_bar, psi);
+    } else {
+        s.G = afsai_build(A, nullptr, cfg.k0, cfg.rho0, cfg.eps0, &psi);
+        Csr Gt = transpose(s.G);
         s.lambda_hat = estimate_lambda_max(s.G, Gt, A, cfg.lanczos_steps, cfg.seed);
         s.omega = compute_omega(s.lambda_hat);
-        ++s.refinement_passes;
         s.exit_reason = SmootherExit::omega_reached;
+        while (s.omega < cfg.omega_bar) {
+            if (!(s.G.nnz_per_row() < rho_bar)) { s.exit_reason = SmootherExit::density_bound; break; }
+            std::vector<double> psi2;
+            Csr G2 = afsai_build(A, &s.G, cfg.ki, cfg.rhoi, cfg.epsi, &psi2);
+            if (G2.nnz() == s.G.nnz()) { s.exit_reason = SmootherExit::pattern_stagnation; break; }
+            s.G = std::move(G2);
+            psi.swap(psi2);
+            Gt = transpose(s.G);
+            s.lambda_hat = estimate_lambda_max(s.G, Gt, A, cfg.lanczos_steps, cfg.seed);
+            s.omega = compute_omega(s.lambda_hat);
+            ++s.refinement_passes;
+            s.exit_reason = SmootherExit::omega_reached;
+        }
     }
     // Kaporin gain (prod A_ii / prod psi_i)^(1/n) in log domain (fsai.hpp:49-51).
     double lg = 0.0;

@@ -203,6 +203,7 @@ class Hierarchy:
             dev = C.c_void_p(int(setup_device)) if setup_device else None
             lib.aspamg_set_srqcg_backend(C.cast(N.gpu().aspamg_gpu_srqcg, C.c_void_p), dev)
             lib.aspamg_set_galerkin_backend(C.cast(N.gpu().aspamg_gpu_galerkin, C.c_void_p), dev)
+            lib.aspamg_set_smoother_backend(C.cast(N.gpu().aspamg_gpu_smoother_setup, C.c_void_p), dev)
         try:
             if coords is not None and len(coords):
                 xyz = np.ascontiguousarray(coords, dtype=np.float64)
@@ -214,6 +215,7 @@ class Hierarchy:
             if setup_device is not None:
                 lib.aspamg_set_srqcg_backend(None, None)
                 lib.aspamg_set_galerkin_backend(None, None)
+                lib.aspamg_set_smoother_backend(None, None)
         return cls(h)
 
     @classmethod
@@ -427,8 +429,8 @@ class GpuVcycle:
 def amg_setup(A: SparseMatrix, coordinates: Optional[np.ndarray] = None, cfg: Optional[N.SetupConfig] = None,
               threads: int = 0, setup_device: Optional[int] = None) -> Hierarchy:
     """SPEC.md:436-444 (produces the hierarchy uploaded once). The setup runs on
-    the CPU; with ``setup_device`` its SRQCG test-space phase and the Galerkin
-    products run on that GPU (bit-identical hierarchy)."""
+    the CPU; with ``setup_device`` its smoother set-up (aFSAI + Lanczos), SRQCG
+    test space and Galerkin products run on that GPU (bit-identical hierarchy)."""
     return Hierarchy.setup(A, coordinates, cfg, threads, setup_device)
 
 
@@ -486,6 +488,42 @@ def gpu_galerkin(P: SparseMatrix, A: SparseMatrix, device: int = 0) -> SparseMat
     if st != 0:
         _raise(st, N.gpu().aspamg_gpu_last_error(None).decode())
     return sink.matrix()
+
+
+def gpu_afsai(A: SparseMatrix, k: int, rho: int, eps: float, device: int = 0):
+    """aFSAI build from the identity start on the GPU (aspamg_gpu_afsai_build);
+    returns (G, psi), bit-identical to the host afsai_build."""
+    sink = _CsrSink()
+    psi = np.empty(max(A.n_rows, 1))
+    av = A.view()
+    st = N.gpu().aspamg_gpu_afsai_build(C.c_void_p(device) if device else None, C.byref(av), k, rho, eps,
+                                        C.cast(sink.fn, C.c_void_p), None, psi.ctypes.data_as(N.P_dbl))
+    if st != 0:
+        _raise(st, N.gpu().aspamg_gpu_last_error(None).decode())
+    return sink.matrix(), psi[: A.n_rows]
+
+
+def gpu_smoother_setup(A: SparseMatrix, cfg: Optional[N.SetupConfig] = None, rho_bar: float = 0.0,
+                       device: int = 0) -> dict:
+    """fsai.cpp smoother_setup (Alg. 3) on the GPU (aspamg_gpu_smoother_setup)."""
+    cfg = cfg or default_config()
+    if rho_bar <= 0.0:
+        a = A.to_scipy().tocoo()
+        rho_bar = 2.0 * float(np.count_nonzero(a.col <= a.row)) / A.n_rows if A.n_rows else 1.0
+    prm = N.SmootherParams(cfg.k0, cfg.rho0, cfg.eps0, cfg.ki, cfg.rhoi, cfg.epsi, cfg.omega_bar, rho_bar,
+                           cfg.lanczos_steps, cfg.seed)
+    sink = _CsrSink()
+    psi = np.empty(max(A.n_rows, 1))
+    om, lam = C.c_double(), C.c_double()
+    passes, ex = C.c_int64(), C.c_int()
+    av = A.view()
+    st = N.gpu().aspamg_gpu_smoother_setup(C.c_void_p(device) if device else None, C.byref(av), C.byref(prm),
+                                           C.cast(sink.fn, C.c_void_p), None, psi.ctypes.data_as(N.P_dbl),
+                                           C.byref(om), C.byref(lam), C.byref(passes), C.byref(ex))
+    if st != 0:
+        _raise(st, N.gpu().aspamg_gpu_last_error(None).decode())
+    return {"G": sink.matrix(), "psi": psi[: A.n_rows], "omega": om.value, "lambda_hat": lam.value,
+            "passes": passes.value, "exit": ex.value}
 
 
 def host_galerkin(P: SparseMatrix, A: SparseMatrix) -> SparseMatrix:

@@ -134,7 +134,7 @@ def test_gpu_srqcg_known_answers(pkg):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg,scale", [(1, 2), (2, 4), (3, 4)])
+@pytest.mark.parametrize("cfg,scale", [(1, 2), (2, 4), (3, 4), (5, 6)])
 def test_gpu_setup_hierarchy_identical(pkg, cfg, scale):
     """amg_setup(..., setup_device=0) == CPU amg_setup, level by level, bit for bit;
     the PCG on it therefore reproduces the CPU-setup solve exactly."""
@@ -240,3 +240,51 @@ def test_gpu_galerkin_errors(pkg):
     P, A = _random_pair(50, 20, 2, 3, 1)
     with pytest.raises(pkg.DimensionError):
         pkg.gpu_galerkin(pkg.SparseMatrix.from_scipy(P[:40]), pkg.SparseMatrix.from_scipy(A))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,rho,eps", [(4, 4, 1e-3), (2, 8, 0.0), (0, 4, 1e-3), (6, 3, 1e-2)])
+def test_gpu_afsai_bit_identical(pkg, k, rho, eps):
+    """aspamg_gpu_afsai_build == the host afsai_build (fsai.cpp), bit for bit, on K
+    and on a dense-row Galerkin operator."""
+    p = pkg.Problem.config(2, 4)
+    h = pkg.amg_setup(p.K, p.coords)
+    for A in (p.K, h.level(1).A):
+        G, psi = pkg.gpu_afsai(A, k, rho, eps)
+        _csr_equal(G, _afsai(pkg, A, k, rho, eps))
+        assert np.all(psi > 0)
+
+
+@pytest.mark.gpu
+def test_gpu_afsai_known_answers(pkg):
+    """SPEC.md:178-180 on the device build."""
+    D = pkg.SparseMatrix.from_scipy(sp.csr_matrix(np.diag(np.arange(1.0, 8.0))))
+    G, _ = pkg.gpu_afsai(D, 3, 4, 1e-3)
+    assert np.allclose(G.to_scipy().toarray(), np.diag(1 / np.sqrt(np.arange(1.0, 8.0))), rtol=1e-15)
+    n = 10
+    T = np.diag(np.full(n, 4.0)) + np.diag(np.full(n - 1, -1.0), 1) + np.diag(np.full(n - 1, -1.0), -1)
+    G, _ = pkg.gpu_afsai(pkg.SparseMatrix.from_scipy(sp.csr_matrix(T)), 20, 20, 0.0)
+    Gd = G.to_scipy().toarray()
+    assert np.abs(Gd @ T @ Gd.T - np.eye(n)).max() <= 1e-10
+
+
+@pytest.mark.gpu
+def test_gpu_afsai_not_spd(pkg):
+    A = pkg.SparseMatrix.from_scipy(sp.csr_matrix(np.array([[1.0, 2.0], [2.0, 1.0]])))
+    with pytest.raises(pkg.NotSpdError):
+        pkg.gpu_afsai(A, 2, 2, 0.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,scale", [(2, 4), (5, 6)])
+def test_gpu_smoother_setup_matches_host(pkg, cfg, scale):
+    """Alg. 3 on the device (aFSAI passes, device transpose, Lanczos) reproduces
+    every level's host smoother: G, omega, lambda_hat, passes, exit reason."""
+    p = pkg.Problem.config(cfg, scale)
+    h = pkg.amg_setup(p.K, p.coords)
+    for l in range(h.n_levels - 1):
+        L = h.level(l)
+        r = pkg.gpu_smoother_setup(L.A)
+        _csr_equal(r["G"], L.G)
+        assert r["omega"] == L.omega and r["lambda_hat"] == L.lambda_hat
+        assert r["passes"] == L.refinement_passes and r["exit"] == L.smoother_exit

@@ -47,9 +47,11 @@ def main():
         hg = P.amg_setup(p.K, p.coords, setup_device=0)
         tg = time.perf_counter() - t
         ic, ig = hc.info(), hg.info()
+        ph = ("T_ts", "T_sm", "T_cs", "T_pl", "T_rap")
         r = {"config": cfg, "scale": a.scale, "n": p.K.n_rows, "cpu_setup_s": tc, "gpu_setup_s": tg,
-             "cpu_T_ts": ic.T_ts, "gpu_T_ts": ig.T_ts, "T_sm": ic.T_sm, "T_cs": ic.T_cs, "T_pl": ic.T_pl,
-             "T_rap": ic.T_rap, "identical": same(hc, hg), "threads": os.cpu_count()}
+             "cpu": {k: getattr(ic, k) for k in ph}, "gpu": {k: getattr(ig, k) for k in ph},
+             "identical": same(hc, hg), "threads": os.cpu_count(),
+             "gpu_phases": "T_sm (aFSAI + Lanczos), T_ts (SRQCG), T_rap (Galerkin) on the GPU; T_cs, T_pl on the CPU"}
         print(json.dumps(r), flush=True)
         res.append(r)
     if a.out:
