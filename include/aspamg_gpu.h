@@ -121,6 +121,9 @@ int aspamg_gpu_galerkin(void* device, const aspamg_csr_view* P, const aspamg_csr
 int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A, const aspamg_smoother_params* prm,
                               aspamg_csr_alloc_fn alloc, void* sink, double* psi, double* omega,
                               double* lambda_hat, int64_t* passes, int* exit_reason);
+/* Returns -1 (declined, nothing written) for operators whose mean row exceeds the
+ * "smoother_max_mean_row" policy (default 128; <= 0 never declines). */
+int aspamg_gpu_set_setup_policy(const char* key, double value);
 /* aFSAI build alone from the identity start, for verification. */
 int aspamg_gpu_afsai_build(void* device, const aspamg_csr_view* A, int64_t k, int64_t rho, double eps,
                            aspamg_csr_alloc_fn alloc, void* sink, double* psi);

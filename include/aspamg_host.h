@@ -56,6 +56,7 @@ typedef struct aspamg_level_view {
     int64_t refinement_passes;
     int32_t smoother_exit; /* 0 omega_reached, 1 density_bound, 2 pattern_stagnation */
     int64_t n_tv;
+    double t_smoother;     /* seconds of this level's smoother set-up (0 after a load) */
 } aspamg_level_view;
 
 typedef struct aspamg_hierarchy_info {
@@ -109,9 +110,10 @@ int aspamg_set_galerkin_backend(aspamg_galerkin_fn fn, void* user);
  * is owned by *out (free with aspamg_csr_free). */
 int aspamg_galerkin(const aspamg_csr_view* P, const aspamg_csr_view* A, aspamg_csr_owned** out,
                     aspamg_csr_view* out_view);
-/* Smoother backend: when set, aspamg_setup runs every level's
+/* Smoother backend: when set, aspamg_setup runs each level's
  * adaptive FSAI set-up through fn (e.g. aspamg_gpu_smoother_setup); the host forms the
- * Kaporin estimate from the returned psi. NULL restores the CPU path. Process-wide. */
+ * Kaporin estimate from the returned psi. fn may return -1 to decline a level (the
+ * host then computes it). NULL restores the CPU path. Process-wide. */
 typedef int (*aspamg_smoother_fn)(void* user, const aspamg_csr_view* A, const aspamg_smoother_params* prm,
                                   aspamg_csr_alloc_fn alloc, void* sink, double* psi, double* omega,
                                   double* lambda_hat, int64_t* passes, int* exit_reason);

@@ -5,7 +5,7 @@ See DESIGN.md for the path, the boundary and the kernels.
 from .solver import (  # noqa: F401
     AspamgError, ConfigError, CudaError, DimensionError, GpuVcycle, Hierarchy, IoError, NotSpdError,
     NumericalError, Problem, SolveReport, SparseMatrix, amg_setup, default_config, gpu_afsai, gpu_galerkin,
-    gpu_smoother_setup, gpu_srqcg,
+    gpu_setup_policy, gpu_smoother_setup, gpu_srqcg,
     host_galerkin, pcg, vcycle_apply,
     SPMV_A, SPMV_G, SPMV_GT, SPMV_P, SPMV_PT,
 )
@@ -13,5 +13,5 @@ from .solver import (  # noqa: F401
 __all__ = [
     "AspamgError", "ConfigError", "CudaError", "DimensionError", "GpuVcycle", "Hierarchy", "IoError",
     "NotSpdError", "NumericalError", "Problem", "SolveReport", "SparseMatrix", "amg_setup", "default_config",
-    "gpu_afsai", "gpu_galerkin", "gpu_smoother_setup", "gpu_srqcg", "host_galerkin", "pcg", "vcycle_apply", "SPMV_A", "SPMV_G", "SPMV_GT", "SPMV_P", "SPMV_PT",
+    "gpu_afsai", "gpu_galerkin", "gpu_setup_policy", "gpu_smoother_setup", "gpu_srqcg", "host_galerkin", "pcg", "vcycle_apply", "SPMV_A", "SPMV_G", "SPMV_GT", "SPMV_P", "SPMV_PT",
 ]

@@ -46,7 +46,7 @@ class SetupConfig(C.Structure):
 class LevelView(C.Structure):
     _fields_ = [("A", CsrView), ("G", CsrView), ("Gt", CsrView), ("P", CsrView), ("Pt", CsrView),
                 ("omega", dbl), ("lambda_hat", dbl), ("kaporin_estimate", dbl),
-                ("refinement_passes", i64), ("smoother_exit", i32), ("n_tv", i64)]
+                ("refinement_passes", i64), ("smoother_exit", i32), ("n_tv", i64), ("t_smoother", dbl)]
 
 
 class HierarchyInfo(C.Structure):
@@ -163,6 +163,7 @@ def gpu() -> C.CDLL:
         lib.aspamg_gpu_srqcg.argtypes = [vp, C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(CsrView), P_dbl, i64, i64,
                                          i64, dbl, C.c_uint64, P_dbl, P_dbl, P_i64, P_i64, C.POINTER(C.c_int)]
         lib.aspamg_gpu_galerkin.argtypes = [vp, C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(CsrView), vp, vp]
+        lib.aspamg_gpu_set_setup_policy.argtypes = [C.c_char_p, dbl]
         lib.aspamg_gpu_afsai_build.argtypes = [vp, C.POINTER(CsrView), i64, i64, dbl, vp, vp, P_dbl]
         lib.aspamg_gpu_smoother_setup.argtypes = [vp, C.POINTER(CsrView), C.POINTER(SmootherParams), vp, vp, P_dbl,
                                                   P_dbl, P_dbl, P_i64, C.POINTER(C.c_int)]

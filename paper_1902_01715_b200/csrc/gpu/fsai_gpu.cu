@@ -600,10 +600,26 @@ double lanczos_device(DevLA& E, const DCsr64& G, const DCsr64& Gt, const DCsr64&
     return 1.05 * ev[(size_t)m - 1];
 }
 
+// Operators whose mean row exceeds this many entries (the coarse Galerkin levels,
+// 200-1000 per row) are declined (status -1) and computed by the host: their
+// factors (m up to ~200) leave one row in flight per SM and their long A rows
+// make every append a long gather, so the host's cached cores are faster there.
+double g_smoother_max_mean_row = 128.0;
+
 }  // namespace
 }  // namespace aspamg_gpu
 
 using namespace aspamg_gpu;
+
+extern "C" int aspamg_gpu_set_setup_policy(const char* key, double value) {
+    const std::string k = key ? key : "";
+    if (k == "smoother_max_mean_row") {
+        g_smoother_max_mean_row = value;
+        return 0;
+    }
+    g_last_err = "set_setup_policy: unknown key " + k;
+    return 4;
+}
 
 // fsai.cpp smoother_setup (Alg. 3) on the device. A: host view; G written through
 // alloc(sink, ...); psi[n] (host) receives the final pass's Schur complements
@@ -614,12 +630,17 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
     aspamg_gpu_ctx* c = nullptr;
     int st = aspamg_gpu_ctx_create((int)(intptr_t)device, &c);
     if (st != 0) return st;
+    bool declined = false;
     st = guard(c, [&] {
         if (!A || !prm || !alloc || !psi_out || !omega || !lambda_hat || !passes || !exit_reason)
             throw Fail{4, "smoother_setup: null argument"};
         if (A->n_rows != A->n_cols) throw Fail{1, "afsai_build: A must be square"};
         const long long n = A->n_rows;
         if (n > INT_MAX) throw Fail{1, "smoother_setup: n exceeds the int32 column range"};
+        if (g_smoother_max_mean_row > 0 && n > 0 && double(A->nnz) / double(n) > g_smoother_max_mean_row) {
+            declined = true;
+            return;
+        }
         long long a_maxrow = 0;
         for (long long i = 0; i < n; ++i) a_maxrow = std::max<long long>(a_maxrow, A->row_offsets[i + 1] - A->row_offsets[i]);
         const DevCsr dA = upload64(c, *A);
@@ -677,7 +698,7 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
         *exit_reason = ex;
     });
     aspamg_gpu_ctx_destroy(c);
-    return st;
+    return (st == 0 && declined) ? -1 : st;
 }
 
 // afsai_build alone (identity start) on the device, for verification.

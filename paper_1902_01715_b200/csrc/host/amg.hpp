@@ -49,7 +49,9 @@ FsaiSmoother smoother_setup(const Csr& A, const SmootherConfig& cfg);  // SPEC.m
 // smoother_setup through the registered external backend (aspamg_set_smoother_backend), if any:
 // returns G, omega, lambda_hat, passes, exit reason, and psi (for the Kaporin estimate).
 bool smoother_backend_set();
-FsaiSmoother smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi);
+// Returns false when the backend declines this operator (status -1): the host path runs instead.
+bool smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi,
+                       FsaiSmoother& out);
 // x' = x + omega G'(G(b - A x)) (host reference; Gt explicit)
 std::vector<double> apply_smoothing_step(const Csr& G, const Csr& Gt, double omega, const Csr& A,
                                          const std::vector<double>& b, const std::vector<double>& x);
@@ -120,6 +122,7 @@ struct Level {
     Csr Gt;                 // explicit G' (transpose, sparse_matrix.cpp:168-189)
     Csr P, Pt;              // absent on the coarsest level
     index_t n_tv = 0;
+    double t_smoother = 0;  // seconds (diagnostic, not persisted)
 };
 
 struct SetupTimings {  // SPEC.md:499 taxonomy (seconds)

@@ -180,6 +180,7 @@ int aspamg_hierarchy_level(const aspamg_hierarchy* hh, int64_t l, aspamg_level_v
         o->refinement_passes = L.smoother.refinement_passes;
         o->smoother_exit = static_cast<int32_t>(L.smoother.exit_reason);
         o->n_tv = L.n_tv;
+        o->t_smoother = L.t_smoother;
     });
 }
 
@@ -354,7 +355,8 @@ namespace aspamg {
 
 bool smoother_backend_set() { return g_smoother_fn != nullptr; }
 
-FsaiSmoother smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi) {
+bool smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi,
+                       FsaiSmoother& out) {
     const aspamg_csr_view a = view(A);
     aspamg_smoother_params prm{cfg.k0, cfg.rho0, cfg.eps0, cfg.ki, cfg.rhoi, cfg.epsi,
                                cfg.omega_bar, rho_bar, cfg.lanczos_steps, cfg.seed};
@@ -364,6 +366,7 @@ FsaiSmoother smoother_external(const Csr& A, const SmootherConfig& cfg, double r
     int exit_reason = 0;
     const int st = g_smoother_fn(g_smoother_user, &a, &prm, csr_sink_alloc, &s.G, psi.data(), &s.omega,
                                  &s.lambda_hat, &passes, &exit_reason);
+    if (st == -1) return false;  // declined: the host computes this level
     if (st != 0) {
         const std::string msg = "smoother backend failed with status " + std::to_string(st);
         if (st == 1) throw DimensionError(msg);
@@ -374,7 +377,8 @@ FsaiSmoother smoother_external(const Csr& A, const SmootherConfig& cfg, double r
     }
     s.refinement_passes = passes;
     s.exit_reason = static_cast<SmootherExit>(exit_reason);
-    return s;
+    out = std::move(s);
+    return true;
 }
 
 }  // namespace aspamg

@@ -233,9 +233,7 @@ FsaiSmoother smoother_setup(const Csr& A, const SmootherConfig& cfg) {
         rho_bar = A.n_rows ? 2.0 * double(lower) / double(A.n_rows) : 1.0;
     }
     std::vector<double> psi;
-    if (smoother_backend_set()) {
-        s = smoother_external(A, cfg, rho_bar, psi);
-    } else {
+    if (!(smoother_backend_set() && smoother_external(A, cfg, rho_bar, psi, s))) {
         s.G = afsai_build(A, nullptr, cfg.k0, cfg.rho0, cfg.eps0, &psi);
         Csr Gt = transpose(s.G);
         s.lambda_hat = estimate_lambda_max(s.G, Gt, A, cfg.lanczos_steps, cfg.seed);

@@ -73,7 +73,8 @@ Hierarchy amg_setup(const Csr& A0, const std::vector<double>& coords, const Hier
         double t = now_s();
         L.smoother = smoother_setup(A, cfg.smoother);
         L.Gt = transpose(L.smoother.G);
-        h.t.T_sm += now_s() - t;
+        L.t_smoother = now_s() - t;
+        h.t.T_sm += L.t_smoother;
         if (lvl == 0) {
             t = now_s();
             Dense rbm;

@@ -180,6 +180,7 @@ class LevelData:
     refinement_passes: int
     smoother_exit: int
     n_tv: int
+    t_smoother: float = 0.0
 
 
 class Hierarchy:
@@ -245,7 +246,7 @@ class Hierarchy:
         lv = self.level_view(l)
         f = lambda v: SparseMatrix.from_view(v, copy)  # noqa: E731
         return LevelData(f(lv.A), f(lv.G), f(lv.Gt), f(lv.P), f(lv.Pt), lv.omega, lv.lambda_hat,
-                         int(lv.refinement_passes), int(lv.smoother_exit), int(lv.n_tv))
+                         int(lv.refinement_passes), int(lv.smoother_exit), int(lv.n_tv), float(lv.t_smoother))
 
     def coarse_factor(self) -> np.ndarray:
         n = C.c_int64()
@@ -520,10 +521,19 @@ def gpu_smoother_setup(A: SparseMatrix, cfg: Optional[N.SetupConfig] = None, rho
     st = N.gpu().aspamg_gpu_smoother_setup(C.c_void_p(device) if device else None, C.byref(av), C.byref(prm),
                                            C.cast(sink.fn, C.c_void_p), None, psi.ctypes.data_as(N.P_dbl),
                                            C.byref(om), C.byref(lam), C.byref(passes), C.byref(ex))
+    if st == -1:
+        return None  # declined by the "smoother_max_mean_row" policy (gpu_setup_policy)
     if st != 0:
         _raise(st, N.gpu().aspamg_gpu_last_error(None).decode())
     return {"G": sink.matrix(), "psi": psi[: A.n_rows], "omega": om.value, "lambda_hat": lam.value,
             "passes": passes.value, "exit": ex.value}
+
+
+def gpu_setup_policy(key: str, value: float) -> None:
+    """Process-wide policy of the GPU setup phases (aspamg_gpu_set_setup_policy)."""
+    st = N.gpu().aspamg_gpu_set_setup_policy(key.encode(), float(value))
+    if st != 0:
+        _raise(st, N.gpu().aspamg_gpu_last_error(None).decode())
 
 
 def host_galerkin(P: SparseMatrix, A: SparseMatrix) -> SparseMatrix:

@@ -136,12 +136,18 @@ def test_gpu_srqcg_known_answers(pkg):
 @pytest.mark.gpu
 @pytest.mark.parametrize("cfg,scale", [(1, 2), (2, 4), (3, 4), (5, 6)])
 def test_gpu_setup_hierarchy_identical(pkg, cfg, scale):
-    """amg_setup(..., setup_device=0) == CPU amg_setup, level by level, bit for bit;
+    """amg_setup(..., setup_device=0) == CPU amg_setup, level by level, bit for bit
+    (with the default level policy and with every level's smoother on the GPU);
     the PCG on it therefore reproduces the CPU-setup solve exactly."""
     p = pkg.Problem.config(cfg, scale)
     h_cpu = pkg.amg_setup(p.K, p.coords)
     h_gpu = pkg.amg_setup(p.K, p.coords, setup_device=0)
     _levels_equal(h_cpu, h_gpu)
+    pkg.gpu_setup_policy("smoother_max_mean_row", 0)
+    try:
+        _levels_equal(h_cpu, pkg.amg_setup(p.K, p.coords, setup_device=0))
+    finally:
+        pkg.gpu_setup_policy("smoother_max_mean_row", 128)
     M1, M2 = pkg.GpuVcycle(h_cpu), pkg.GpuVcycle(h_gpu)
     x1, r1 = pkg.pcg(p.K, p.rhs, M1)
     x2, r2 = pkg.pcg(p.K, p.rhs, M2)
@@ -276,15 +282,29 @@ def test_gpu_afsai_not_spd(pkg):
 
 
 @pytest.mark.gpu
+def test_gpu_smoother_policy_declines_long_rows(pkg):
+    """Operators with long rows are declined (-1 -> None) under the default policy."""
+    p = pkg.Problem.config(2, 4)
+    h = pkg.amg_setup(p.K, p.coords)
+    assert pkg.gpu_smoother_setup(h.level(1).A) is None   # Galerkin operator, ~180 entries per row
+    assert pkg.gpu_smoother_setup(p.K) is not None        # K, <= 81 entries per row
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("cfg,scale", [(2, 4), (5, 6)])
 def test_gpu_smoother_setup_matches_host(pkg, cfg, scale):
     """Alg. 3 on the device (aFSAI passes, device transpose, Lanczos) reproduces
     every level's host smoother: G, omega, lambda_hat, passes, exit reason."""
     p = pkg.Problem.config(cfg, scale)
     h = pkg.amg_setup(p.K, p.coords)
+    pkg.gpu_setup_policy("smoother_max_mean_row", 0)  # never decline: exercise the device path on every level
+    try:
+        rs = [pkg.gpu_smoother_setup(h.level(l).A) for l in range(h.n_levels - 1)]
+    finally:
+        pkg.gpu_setup_policy("smoother_max_mean_row", 128)
     for l in range(h.n_levels - 1):
         L = h.level(l)
-        r = pkg.gpu_smoother_setup(L.A)
+        r = rs[l]
         _csr_equal(r["G"], L.G)
         assert r["omega"] == L.omega and r["lambda_hat"] == L.lambda_hat
         assert r["passes"] == L.refinement_passes and r["exit"] == L.smoother_exit

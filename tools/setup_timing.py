@@ -34,8 +34,11 @@ def main():
     ap.add_argument("--configs", default="2")
     ap.add_argument("--scale", type=int, default=1)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--smoother-max-mean-row", type=float, default=128.0,
+                    help="GPU smoother level policy (0 = every level on the GPU)")
     a = ap.parse_args()
     res = []
+    P.gpu_setup_policy("smoother_max_mean_row", a.smoother_max_mean_row)
     for cfg in [int(c) for c in a.configs.split(",")]:
         p = P.Problem.config(cfg, a.scale)
         warm = P.Problem.config(1, 4)
@@ -51,6 +54,10 @@ def main():
         r = {"config": cfg, "scale": a.scale, "n": p.K.n_rows, "cpu_setup_s": tc, "gpu_setup_s": tg,
              "cpu": {k: getattr(ic, k) for k in ph}, "gpu": {k: getattr(ig, k) for k in ph},
              "identical": same(hc, hg), "threads": os.cpu_count(),
+             "smoother_max_mean_row": a.smoother_max_mean_row,
+             "levels": [{"n": int(hc.level(l).A.n_rows), "nnz_row": hc.level(l).A.nnz / max(hc.level(l).A.n_rows, 1),
+                         "passes": hc.level(l).refinement_passes, "cpu_t_sm": hc.level(l).t_smoother,
+                         "gpu_t_sm": hg.level(l).t_smoother} for l in range(hc.n_levels - 1)],
              "gpu_phases": "T_sm (aFSAI + Lanczos), T_ts (SRQCG), T_rap (Galerkin) on the GPU; T_cs, T_pl on the CPU"}
         print(json.dumps(r), flush=True)
         res.append(r)
