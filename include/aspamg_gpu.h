@@ -121,8 +121,12 @@ int aspamg_gpu_galerkin(void* device, const aspamg_csr_view* P, const aspamg_csr
 int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A, const aspamg_smoother_params* prm,
                               aspamg_csr_alloc_fn alloc, void* sink, double* psi, double* omega,
                               double* lambda_hat, int64_t* passes, int* exit_reason);
-/* Returns -1 (declined, nothing written) for operators whose mean row exceeds the
- * "smoother_max_mean_row" policy (default 128; <= 0 never declines). */
+/* Level policy of aspamg_gpu_smoother_setup (process-wide):
+ *   "smoother_max_mean_row" (300), "smoother_min_rows" (50000): operators with longer mean
+ *      rows or fewer rows are declined (returns -1, nothing written);
+ *   "smoother_max_pattern" (64): before a refinement pass whose pattern bound exceeds it,
+ *      returns -2 with the state after the last finished pass (G, psi, omega, lambda,
+ *      passes); the caller continues the refinement loop. <= 0 disables a rule. */
 int aspamg_gpu_set_setup_policy(const char* key, double value);
 /* aFSAI build alone from the identity start, for verification. */
 int aspamg_gpu_afsai_build(void* device, const aspamg_csr_view* A, int64_t k, int64_t rho, double eps,

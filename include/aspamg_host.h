@@ -113,7 +113,8 @@ int aspamg_galerkin(const aspamg_csr_view* P, const aspamg_csr_view* A, aspamg_c
 /* Smoother backend: when set, aspamg_setup runs each level's
  * adaptive FSAI set-up through fn (e.g. aspamg_gpu_smoother_setup); the host forms the
  * Kaporin estimate from the returned psi. fn may return -1 to decline a level (the
- * host then computes it). NULL restores the CPU path. Process-wide. */
+ * host then computes it) or -2 to hand back the refinement loop after its last finished
+ * pass (the host continues it). NULL restores the CPU path. Process-wide. */
 typedef int (*aspamg_smoother_fn)(void* user, const aspamg_csr_view* A, const aspamg_smoother_params* prm,
                                   aspamg_csr_alloc_fn alloc, void* sink, double* psi, double* omega,
                                   double* lambda_hat, int64_t* passes, int* exit_reason);

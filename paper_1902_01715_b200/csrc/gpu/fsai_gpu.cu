@@ -600,11 +600,18 @@ double lanczos_device(DevLA& E, const DCsr64& G, const DCsr64& Gt, const DCsr64&
     return 1.05 * ev[(size_t)m - 1];
 }
 
-// Operators whose mean row exceeds this many entries (the coarse Galerkin levels,
-// 200-1000 per row) are declined (status -1) and computed by the host: their
-// factors (m up to ~200) leave one row in flight per SM and their long A rows
-// make every append a long gather, so the host's cached cores are faster there.
-double g_smoother_max_mean_row = 128.0;
+// Level policy (measured, profiles/setup_timing_*.json). The exact per-row
+// restatement keeps each row's factor (m(m+1)/2 doubles) and gradient table on
+// chip, so rows in flight per SM fall as m^2 and every append walks an A row:
+//  * operators with mean rows above smoother_max_mean_row (the dense coarse
+//    Galerkin levels) or fewer than smoother_min_rows rows are declined
+//    (status -1): the host computes them;
+//  * refinement passes whose pattern bound would exceed smoother_max_pattern
+//    are handed back (status -2, state after the last finished pass): the host
+//    continues the same loop from there — bit-identical either way.
+double g_smoother_max_mean_row = 300.0;
+double g_smoother_min_rows = 50000.0;
+double g_smoother_max_pattern = 64.0;
 
 }  // namespace
 }  // namespace aspamg_gpu
@@ -615,6 +622,14 @@ extern "C" int aspamg_gpu_set_setup_policy(const char* key, double value) {
     const std::string k = key ? key : "";
     if (k == "smoother_max_mean_row") {
         g_smoother_max_mean_row = value;
+        return 0;
+    }
+    if (k == "smoother_min_rows") {
+        g_smoother_min_rows = value;
+        return 0;
+    }
+    if (k == "smoother_max_pattern") {
+        g_smoother_max_pattern = value;
         return 0;
     }
     g_last_err = "set_setup_policy: unknown key " + k;
@@ -630,14 +645,15 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
     aspamg_gpu_ctx* c = nullptr;
     int st = aspamg_gpu_ctx_create((int)(intptr_t)device, &c);
     if (st != 0) return st;
-    bool declined = false;
+    bool declined = false, handed = false;
     st = guard(c, [&] {
         if (!A || !prm || !alloc || !psi_out || !omega || !lambda_hat || !passes || !exit_reason)
             throw Fail{4, "smoother_setup: null argument"};
         if (A->n_rows != A->n_cols) throw Fail{1, "afsai_build: A must be square"};
         const long long n = A->n_rows;
         if (n > INT_MAX) throw Fail{1, "smoother_setup: n exceeds the int32 column range"};
-        if (g_smoother_max_mean_row > 0 && n > 0 && double(A->nnz) / double(n) > g_smoother_max_mean_row) {
+        if ((g_smoother_max_mean_row > 0 && n > 0 && double(A->nnz) / double(n) > g_smoother_max_mean_row) ||
+            double(n) < g_smoother_min_rows) {
             declined = true;
             return;
         }
@@ -662,6 +678,14 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
         int64_t np = 0;
         int ex = 0;  // omega_reached
         while (om < prm->omega_bar) {
+            if (g_smoother_max_pattern > 0) {  // hand the remaining passes to the host?
+                long long gmax = 0;
+                for (long long i = 0; i < n; ++i) gmax = std::max(gmax, G.rp[(size_t)i + 1] - G.rp[(size_t)i]);
+                if (double(gmax + prm->ki * prm->rhoi + 1) > g_smoother_max_pattern) {
+                    handed = true;
+                    break;
+                }
+            }
             const double nnz_r = n ? double(G.d.view.nnz) / double(n) : 0.0;
             if (!(nnz_r < prm->rho_bar)) { ex = 1; break; }  // density_bound
             DevG G2 = afsai_device(c, dA.view, a_maxrow, &G, (int)prm->ki, (int)prm->rhoi, prm->epsi, psi2);
@@ -698,7 +722,7 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
         *exit_reason = ex;
     });
     aspamg_gpu_ctx_destroy(c);
-    return (st == 0 && declined) ? -1 : st;
+    return (st == 0 && declined) ? -1 : (st == 0 && handed) ? -2 : st;
 }
 
 // afsai_build alone (identity start) on the device, for verification.

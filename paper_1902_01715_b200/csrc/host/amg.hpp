@@ -49,9 +49,10 @@ FsaiSmoother smoother_setup(const Csr& A, const SmootherConfig& cfg);  // SPEC.m
 // smoother_setup through the registered external backend (aspamg_set_smoother_backend), if any:
 // returns G, omega, lambda_hat, passes, exit reason, and psi (for the Kaporin estimate).
 bool smoother_backend_set();
-// Returns false when the backend declines this operator (status -1): the host path runs instead.
-bool smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi,
-                       FsaiSmoother& out);
+// 0: the backend declined (status -1), the host computes the level; 1: complete;
+// 2: handed back after a finished pass (status -2), the host continues the refinement loop.
+int smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi,
+                      FsaiSmoother& out);
 // x' = x + omega G'(G(b - A x)) (host reference; Gt explicit)
 std::vector<double> apply_smoothing_step(const Csr& G, const Csr& Gt, double omega, const Csr& A,
                                          const std::vector<double>& b, const std::vector<double>& x);

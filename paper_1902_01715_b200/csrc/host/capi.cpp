@@ -355,8 +355,8 @@ namespace aspamg {
 
 bool smoother_backend_set() { return g_smoother_fn != nullptr; }
 
-bool smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi,
-                       FsaiSmoother& out) {
+int smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi,
+                      FsaiSmoother& out) {
     const aspamg_csr_view a = view(A);
     aspamg_smoother_params prm{cfg.k0, cfg.rho0, cfg.eps0, cfg.ki, cfg.rhoi, cfg.epsi,
                                cfg.omega_bar, rho_bar, cfg.lanczos_steps, cfg.seed};
@@ -366,8 +366,8 @@ bool smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, 
     int exit_reason = 0;
     const int st = g_smoother_fn(g_smoother_user, &a, &prm, csr_sink_alloc, &s.G, psi.data(), &s.omega,
                                  &s.lambda_hat, &passes, &exit_reason);
-    if (st == -1) return false;  // declined: the host computes this level
-    if (st != 0) {
+    if (st == -1) return 0;  // declined: the host computes this level
+    if (st != 0 && st != -2) {
         const std::string msg = "smoother backend failed with status " + std::to_string(st);
         if (st == 1) throw DimensionError(msg);
         if (st == 2) throw NotSpdError(msg);
@@ -378,7 +378,7 @@ bool smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, 
     s.refinement_passes = passes;
     s.exit_reason = static_cast<SmootherExit>(exit_reason);
     out = std::move(s);
-    return true;
+    return st == -2 ? 2 : 1;
 }
 
 }  // namespace aspamg

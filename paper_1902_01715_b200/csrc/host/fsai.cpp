@@ -233,12 +233,16 @@ FsaiSmoother smoother_setup(const Csr& A, const SmootherConfig& cfg) {
         rho_bar = A.n_rows ? 2.0 * double(lower) / double(A.n_rows) : 1.0;
     }
     std::vector<double> psi;
-    if (!(smoother_backend_set() && smoother_external(A, cfg, rho_bar, psi, s))) {
-        s.G = afsai_build(A, nullptr, cfg.k0, cfg.rho0, cfg.eps0, &psi);
-        Csr Gt = transpose(s.G);
-        s.lambda_hat = estimate_lambda_max(s.G, Gt, A, cfg.lanczos_steps, cfg.seed);
-        s.omega = compute_omega(s.lambda_hat);
-        s.exit_reason = SmootherExit::omega_reached;
+    const int ext = smoother_backend_set() ? smoother_external(A, cfg, rho_bar, psi, s) : 0;
+    if (ext != 1) {
+        Csr Gt;
+        if (ext == 0) {
+            s.G = afsai_build(A, nullptr, cfg.k0, cfg.rho0, cfg.eps0, &psi);
+            Gt = transpose(s.G);
+            s.lambda_hat = estimate_lambda_max(s.G, Gt, A, cfg.lanczos_steps, cfg.seed);
+            s.omega = compute_omega(s.lambda_hat);
+            s.exit_reason = SmootherExit::omega_reached;
+        }  // ext == 2: the backend finished some passes; continue its loop from there
         while (s.omega < cfg.omega_bar) {
             if (!(s.G.nnz_per_row() < rho_bar)) { s.exit_reason = SmootherExit::density_bound; break; }
             std::vector<double> psi2;

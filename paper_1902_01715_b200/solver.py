@@ -522,11 +522,11 @@ def gpu_smoother_setup(A: SparseMatrix, cfg: Optional[N.SetupConfig] = None, rho
                                            C.cast(sink.fn, C.c_void_p), None, psi.ctypes.data_as(N.P_dbl),
                                            C.byref(om), C.byref(lam), C.byref(passes), C.byref(ex))
     if st == -1:
-        return None  # declined by the "smoother_max_mean_row" policy (gpu_setup_policy)
-    if st != 0:
+        return None  # declined by the level policy (gpu_setup_policy)
+    if st not in (0, -2):
         _raise(st, N.gpu().aspamg_gpu_last_error(None).decode())
     return {"G": sink.matrix(), "psi": psi[: A.n_rows], "omega": om.value, "lambda_hat": lam.value,
-            "passes": passes.value, "exit": ex.value}
+            "passes": passes.value, "exit": ex.value, "handed_back": st == -2}
 
 
 def gpu_setup_policy(key: str, value: float) -> None:

@@ -50,6 +50,17 @@ def _levels_equal(h1, h2):
     assert np.array_equal(h1.coarse_factor(), h2.coarse_factor())
 
 
+def _all_gpu(pkg):
+    for k in ("smoother_max_mean_row", "smoother_min_rows", "smoother_max_pattern"):
+        pkg.gpu_setup_policy(k, 0)
+
+
+def _default_policy(pkg):
+    pkg.gpu_setup_policy("smoother_max_mean_row", 300)
+    pkg.gpu_setup_policy("smoother_min_rows", 50000)
+    pkg.gpu_setup_policy("smoother_max_pattern", 64)
+
+
 def test_srqcg_backend_hook_cpu(pkg):
     """The external test-space hook (aspamg_set_srqcg_backend) on the CPU: a
     backend that forwards to the host restatement reproduces the built-in path
@@ -143,11 +154,17 @@ def test_gpu_setup_hierarchy_identical(pkg, cfg, scale):
     h_cpu = pkg.amg_setup(p.K, p.coords)
     h_gpu = pkg.amg_setup(p.K, p.coords, setup_device=0)
     _levels_equal(h_cpu, h_gpu)
-    pkg.gpu_setup_policy("smoother_max_mean_row", 0)
+    _all_gpu(pkg)
     try:
         _levels_equal(h_cpu, pkg.amg_setup(p.K, p.coords, setup_device=0))
     finally:
-        pkg.gpu_setup_policy("smoother_max_mean_row", 128)
+        _default_policy(pkg)
+    pkg.gpu_setup_policy("smoother_max_pattern", 24)  # hand back after the first refinement passes
+    pkg.gpu_setup_policy("smoother_min_rows", 0)
+    try:
+        _levels_equal(h_cpu, pkg.amg_setup(p.K, p.coords, setup_device=0))
+    finally:
+        _default_policy(pkg)
     M1, M2 = pkg.GpuVcycle(h_cpu), pkg.GpuVcycle(h_gpu)
     x1, r1 = pkg.pcg(p.K, p.rhs, M1)
     x2, r2 = pkg.pcg(p.K, p.rhs, M2)
@@ -283,11 +300,17 @@ def test_gpu_afsai_not_spd(pkg):
 
 @pytest.mark.gpu
 def test_gpu_smoother_policy_declines_long_rows(pkg):
-    """Operators with long rows are declined (-1 -> None) under the default policy."""
+    """Level policy: small operators are declined (-1 -> None); a pattern bound
+    below the refinement growth hands the loop back after finished passes."""
     p = pkg.Problem.config(2, 4)
-    h = pkg.amg_setup(p.K, p.coords)
-    assert pkg.gpu_smoother_setup(h.level(1).A) is None   # Galerkin operator, ~180 entries per row
-    assert pkg.gpu_smoother_setup(p.K) is not None        # K, <= 81 entries per row
+    assert pkg.gpu_smoother_setup(p.K) is None            # 13,872 rows < smoother_min_rows
+    pkg.gpu_setup_policy("smoother_min_rows", 0)
+    pkg.gpu_setup_policy("smoother_max_pattern", 20)
+    try:
+        r = pkg.gpu_smoother_setup(p.K)
+    finally:
+        _default_policy(pkg)
+    assert r is not None and r["handed_back"] and r["passes"] == 0
 
 
 @pytest.mark.gpu
@@ -297,11 +320,11 @@ def test_gpu_smoother_setup_matches_host(pkg, cfg, scale):
     every level's host smoother: G, omega, lambda_hat, passes, exit reason."""
     p = pkg.Problem.config(cfg, scale)
     h = pkg.amg_setup(p.K, p.coords)
-    pkg.gpu_setup_policy("smoother_max_mean_row", 0)  # never decline: exercise the device path on every level
+    _all_gpu(pkg)  # never decline or hand back: exercise the device path on every level
     try:
         rs = [pkg.gpu_smoother_setup(h.level(l).A) for l in range(h.n_levels - 1)]
     finally:
-        pkg.gpu_setup_policy("smoother_max_mean_row", 128)
+        _default_policy(pkg)
     for l in range(h.n_levels - 1):
         L = h.level(l)
         r = rs[l]
