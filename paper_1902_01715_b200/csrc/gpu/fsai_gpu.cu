@@ -55,15 +55,24 @@ struct AfsaiArgs {
 
 __host__ __device__ inline size_t packed(long long m) { return (size_t)m * (size_t)(m + 1) / 2; }
 
+// pattern-position table: column -> index in the pattern (power of two >= 2 mcap)
+__host__ __device__ inline int pat_cap(int mcap) {
+    int c = 64;
+    while (c < 2 * mcap) c <<= 1;
+    return c;
+}
+
 __host__ __device__ inline size_t warp_bytes(int mcap, int hcap, bool l_global) {
     const size_t lp = l_global ? 0 : packed(mcap);
-    size_t b = 8 * (lp + 3 * (size_t)mcap + (size_t)hcap) + 4 * ((size_t)hcap + (size_t)mcap + 40);
+    size_t b = 8 * (lp + 3 * (size_t)mcap + (size_t)hcap) +
+               4 * ((size_t)hcap + (size_t)mcap + 40 + 2 * (size_t)pat_cap(mcap));
     return (b + 15) & ~(size_t)15;
 }
 
 struct WarpMem {
     double *L, *y, *a, *pr, *hv;
-    int *hk, *pat, *sel;
+    int *hk, *pat, *sel, *pk, *pv;
+    int pcap;
 };
 
 __device__ __forceinline__ unsigned hslot(int j, int cap) { return ((unsigned)j * 2654435761u) & (unsigned)(cap - 1); }
@@ -118,13 +127,47 @@ __device__ void trsv_lower_t_w(int n, const double* L, double* b, double* pr, in
     }
 }
 
+__device__ void pat_insert(const WarpMem& w, int col, int q) {  // one lane
+    unsigned h = hslot(col, w.pcap);
+    while (w.pk[h] != -1) h = (h + 1) & (unsigned)(w.pcap - 1);
+    w.pk[h] = col;
+    w.pv[h] = q;
+}
+__device__ int pat_find(const WarpMem& w, long long col) {
+    unsigned h = hslot((int)col, w.pcap);
+    for (;;) {
+        const int k = w.pk[h];
+        if (k == (int)col) return w.pv[h];
+        if (k == -1) return -1;
+        h = (h + 1) & (unsigned)(w.pcap - 1);
+    }
+}
+
+// out[q] = A(r, pat[q]) for q < m (0 if not stored: the host's dense scatter),
+// one coalesced pass over row r; returns A(r, d) on every lane.
+__device__ double gather_row(const DCsr64& A, long long r, long long d, const WarpMem& w, int m, double* out, int lane) {
+    for (int q = lane; q < m; q += 32) out[q] = 0.0;
+    __syncwarp();
+    double dv = 0.0;
+    bool hit = false;
+    for (long long e = A.rp[r] + lane; e < A.rp[r + 1]; e += 32) {
+        const long long c = A.ci[e];
+        if (c == d) {
+            dv = A.v[e];
+            hit = true;
+        }
+        const int q = pat_find(w, c);
+        if (q >= 0 && q < m) out[q] = A.v[e];
+    }
+    __syncwarp();
+    const unsigned b = __ballot_sync(FULL, hit);
+    return b ? __shfl_sync(FULL, dv, __ffs(b) - 1) : 0.0;
+}
+
 // fsai.cpp chol_append: row m of the factor from A[j, pat[0..m)].
 __device__ bool chol_append_w(const DCsr64& A, const WarpMem& w, int m, long long j, int lane) {
     double* row = w.L + packed(m);
-    for (int q = lane; q < m; q += 32) row[q] = a_at(A, j, w.pat[q]);
-    double ajj = lane == 0 ? a_at(A, j, j) : 0.0;
-    ajj = __shfl_sync(FULL, ajj, 0);
-    __syncwarp();
+    const double ajj = gather_row(A, j, j, w, m, row, lane);
     trsv_lower_w(m, w.L, row, lane);
     const double d = __dsub_rn(ajj, dot4w(row, row, m, lane));
     if (!(d > 0.0)) return false;
@@ -181,6 +224,8 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
     const DCsr64& A = P.A;
     int m = 0;
     bool ok = true;
+    for (int q = lane; q < w.pcap; q += 32) w.pk[q] = -1;
+    __syncwarp();
     if (P.gs_rp) {
         const long long b = P.gs_rp[i], e = P.gs_rp[i + 1];
         int ns = 0;
@@ -194,6 +239,8 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
         }
         __syncwarp();
         for (int q = 0; q < ns; ++q) {
+            if (lane == 0) pat_insert(w, w.pat[q], q);
+            __syncwarp();
             if (!chol_append_w(A, w, m, w.pat[q], lane)) {
                 ok = false;
                 break;
@@ -207,11 +254,8 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
     bool ovf = false;
     for (int step = 0; ok; ++step) {
         // bordered solve y = A_PP^{-1} a, psi = a_ii - a'y
-        for (int q = lane; q < m; q += 32) {
-            const double v = a_at(A, i, w.pat[q]);
-            w.a[q] = v;
-            w.y[q] = v;
-        }
+        gather_row(A, i, i, w, m, w.a, lane);
+        for (int q = lane; q < m; q += 32) w.y[q] = w.a[q];
         __syncwarp();
         trsv_lower_w(m, w.L, w.y, lane);
         trsv_lower_t_w(m, w.L, w.y, w.pr, lane);
@@ -285,7 +329,10 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
         __syncwarp();
         for (int c = 0; c < take && ok; ++c) {
             const int j = w.sel[c];
-            if (lane == 0) w.pat[m] = j;
+            if (lane == 0) {
+                w.pat[m] = j;
+                pat_insert(w, j, m);
+            }
             __syncwarp();
             if (!chol_append_w(A, w, m, j, lane)) ok = false;
             else ++m;
@@ -339,6 +386,9 @@ __global__ void k_afsai(const AfsaiArgs P) {
     w.hk = reinterpret_cast<int*>(w.hv + P.hcap);
     w.pat = w.hk + P.hcap;
     w.sel = w.pat + P.mcap;
+    w.pcap = pat_cap(P.mcap);
+    w.pk = w.sel + 40;
+    w.pv = w.pk + w.pcap;
     const long long total = P.rows ? P.nrows : P.A.n_rows;
     for (long long t = (long long)blockIdx.x * W + wid; t < total; t += (long long)gridDim.x * W)
         afsai_row(P, w, P.rows ? P.rows[t] : t, lane);
