@@ -256,7 +256,9 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
             CK(cudaMemcpy(S.perm, perm.data(), perm.size() * sizeof(int), cudaMemcpyHostToDevice));
         }
         S.pol = (long long)(12.0 * nnz) > c->opt_stream_bytes ? 1 : 0;
-        S.u = c->opt_sell_u > 0 ? (int)c->opt_sell_u : (maxlen <= 4 ? 41 : 83);  // U*10 + min CTAs/SM
+        // U*10 + min CTAs/SM. Large operators: U = 4 at 4 CTAs/SM (64 registers) keeps more
+        // warps in flight (C2 level-0 G: 35 vs 40 us); smaller ones keep U = 8 (tools/tune_kernels.py)
+        S.u = c->opt_sell_u > 0 ? (int)c->opt_sell_u : (maxlen <= 4 ? 41 : v.n_rows >= 400000 ? 44 : 83);
         S.tma = (int)c->opt_sell_tma;  // SEG*10 + stages, 0 = register pipeline
         return M;
     }
