@@ -382,23 +382,33 @@ __device__ __forceinline__ SellChunk sell_chunk(const DSell& M, int ch, int lane
     return c;
 }
 
-template <int STREAM, bool I16>
-__device__ __forceinline__ int sell_col(const DSell& M, long long idx) {
-    if constexpr (I16) return ld_mat<STREAM>(M.ci16 + idx);
-    else return ld_mat<STREAM>(M.ci + idx);
-}
+template <bool I16>
+struct SellCol {
+    using T = int;
+    __device__ static const T* base(const DSell& M) { return M.ci; }
+};
+template <>
+struct SellCol<true> {
+    using T = unsigned short;
+    __device__ static const T* base(const DSell& M) { return M.ci16; }
+};
 
-template <int U, int STREAM, int MINB, bool I16>
+// CHH: the layout's chunk height when known at compile time (32), 0 = runtime
+// (M.chh): with a constant slot stride every load of a group addresses off one
+// running pointer with an immediate offset.
+template <int U, int STREAM, int MINB, bool I16, int CHH>
 __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const double* __restrict__ x, double* y,
                                                   const double* aux, double omega, const double* dotw, Red red,
                                                   const int* done) {
     pdl_enter();
     if (is_done(done)) return;
+    using CT = typename SellCol<I16>::T;
+    const CT* __restrict__ colb = SellCol<I16>::base(M);
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * kBlock) >> 5;
     const bool need_aux = epi == EPI_RESID || epi == EPI_ADD || epi == EPI_ADDSCALE;
-    const long long SS = M.chh;  // slot stride
+    const int SS = CHH ? CHH : M.chh;  // slot stride
     double dacc = 0.0;
     int ch = warp;
     SellChunk nx{};
@@ -407,35 +417,40 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const d
     for (int u = 0; u < U; ++u) cn[u] = 0;
     if (ch < M.nchunks) {
         nx = sell_chunk<STREAM>(M, ch, lane, need_aux, aux, dotw);
+        const CT* cp = colb + nx.base;
 #pragma unroll
-        for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? sell_col<STREAM, I16>(M, nx.base + SS * u) : 0;
+        for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? (int)ld_mat<STREAM>(cp + SS * u) : 0;
     }
     while (ch < M.nchunks) {
         const SellChunk cu = nx;
         const int chn = ch + nwarps;
         if (chn < M.nchunks) nx = sell_chunk<STREAM>(M, chn, lane, need_aux, aux, dotw);
+        const double* vp = M.v + cu.base;  // slot j of this lane at vp[SS * j]
+        const CT* cp = colb + cu.base;
+        const double* xb = x + cu.cb;
+        int rem = cu.len;                  // entries of this row not yet consumed
         double s = 0.0;
-        for (int j0 = 0; j0 < cu.w; j0 += U) {
+        for (int j0 = 0; j0 < cu.w; j0 += U, vp += SS * U, cp += SS * U, rem -= U) {
             int cc[U];
             double v[U], xv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 cc[u] = cn[u];
-                const bool p = j0 + u < cu.len;
-                v[u] = p ? ld_mat<STREAM>(M.v + cu.base + SS * (j0 + u)) : 0.0;
-                xv[u] = p ? __ldg(x + cu.cb + cc[u]) : 0.0;
+                const bool p = u < rem;
+                v[u] = p ? ld_mat<STREAM>(vp + SS * u) : 0.0;
+                xv[u] = p ? __ldg(xb + cc[u]) : 0.0;
             }
             if (j0 + U < cu.w) {
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    cn[u] = (j0 + U + u < cu.len) ? sell_col<STREAM, I16>(M, cu.base + SS * (j0 + U + u)) : 0;
+                for (int u = 0; u < U; ++u) cn[u] = (U + u < rem) ? (int)ld_mat<STREAM>(cp + SS * (U + u)) : 0;
             } else if (chn < M.nchunks) {
+                const CT* np = colb + nx.base;
 #pragma unroll
-                for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? sell_col<STREAM, I16>(M, nx.base + SS * u) : 0;
+                for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? (int)ld_mat<STREAM>(np + SS * u) : 0;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if (j0 + u < cu.len) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+                if (u < rem) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
         }
         if (cu.act) {
             double out;
@@ -891,7 +906,9 @@ int occ_grid(K kern, long long work_units_per_cta_needed, size_t smem = 0) {
 
 // ------------------------------------------------------------------ host API
 // Kernel pointer for an operand's index width (same signature either way).
-#define SELLK(UU, P, MB) (M.sell.ci16 ? k_sell<UU, P, MB, true> : k_sell<UU, P, MB, false>)
+#define SELLK(UU, P, MB)                                                                            \
+    (M.sell.chh == 32 ? (M.sell.ci16 ? k_sell<UU, P, MB, true, 32> : k_sell<UU, P, MB, false, 32>)   \
+                      : (M.sell.ci16 ? k_sell<UU, P, MB, true, 0> : k_sell<UU, P, MB, false, 0>))
 #define CSRK(GG, P) (M.csr.ci16 ? k_csr<GG, P, true> : k_csr<GG, P, false>)
 
 int spmv_grid(const DMat& M) {
