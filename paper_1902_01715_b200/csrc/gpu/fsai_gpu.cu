@@ -150,14 +150,26 @@ __device__ double gather_row(const DCsr64& A, long long r, long long d, const Wa
     __syncwarp();
     double dv = 0.0;
     bool hit = false;
-    for (long long e = A.rp[r] + lane; e < A.rp[r + 1]; e += 32) {
-        const long long c = A.ci[e];
-        if (c == d) {
-            dv = A.v[e];
-            hit = true;
+    const long long b = A.rp[r], e1 = A.rp[r + 1];
+    for (long long e0 = b + lane; e0 < e1; e0 += 4 * 32) {  // 4 loads in flight per lane
+        long long c[4];
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long e = e0 + 32 * u;
+            c[u] = e < e1 ? A.ci[e] : -1;
+            v[u] = e < e1 ? A.v[e] : 0.0;
         }
-        const int q = pat_find(w, c);
-        if (q >= 0 && q < m) out[q] = A.v[e];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (c[u] < 0) continue;
+            if (c[u] == d) {
+                dv = v[u];
+                hit = true;
+            }
+            const int q = pat_find(w, c[u]);
+            if (q >= 0 && q < m) out[q] = v[u];
+        }
     }
     __syncwarp();
     const unsigned b = __ballot_sync(FULL, hit);
