@@ -172,8 +172,8 @@ __device__ double gather_row(const DCsr64& A, long long r, long long d, const Wa
         }
     }
     __syncwarp();
-    const unsigned b = __ballot_sync(FULL, hit);
-    return b ? __shfl_sync(FULL, dv, __ffs(b) - 1) : 0.0;
+    const unsigned hb = __ballot_sync(FULL, hit);
+    return hb ? __shfl_sync(FULL, dv, __ffs(hb) - 1) : 0.0;
 }
 
 // fsai.cpp chol_append: row m of the factor from A[j, pat[0..m)].
