@@ -94,6 +94,7 @@ __device__ double dot4w(const double* x, const double* y, int n, int lane) {
     double s = 0.0;
     const int n4 = n & ~3;
     if (lane < 4) {
+#pragma unroll 4
         for (int k = lane; k < n4; k += 4) s = __dadd_rn(s, __dmul_rn(x[k], y[k]));
         if (lane == 0)
             for (int k = n4; k < n; ++k) s = __dadd_rn(s, __dmul_rn(x[k], y[k]));
@@ -120,6 +121,7 @@ __device__ void trsv_lower_t_w(int n, const double* L, double* b, double* pr, in
         __syncwarp();
         if (lane == 0) {
             double s = b[i];
+#pragma unroll 4
             for (int k = i + 1; k < n; ++k) s = __dsub_rn(s, pr[k]);
             b[i] = __ddiv_rn(s, L[packed(i) + i]);
         }
