@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--scale", type=int, default=1)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "full_configs.json"))
     ap.add_argument("--oracle", type=int, default=1, help="run the CPU oracle solve (0 = GPU only)")
+    ap.add_argument("--max-it", type=int, default=1000,
+                    help="PCG iteration cap (the paper's 1000, PAPER.md:1211; C4 needs more at full size)")
     ap.add_argument("--gpu-setup", type=int, default=0, help="SRQCG + Galerkin on the GPU (bit-identical hierarchy)")
     args = ap.parse_args()
 
@@ -53,12 +55,12 @@ def main():
                "gen_s": t_gen, "gpu_setup": bool(args.gpu_setup),
                "setup_phases": {k: getattr(info, k) for k in ("T_ts", "T_sm", "T_cs", "T_pl", "T_rap")},
                "levels": int(info.n_levels), "C_gd": info.C_gd, "C_op": info.C_op, "C_fs": info.C_fs,
-               "level_sizes": [int(h.level_view(l).A.n_rows) for l in range(info.n_levels)]}
+               "max_it": args.max_it, "level_sizes": [int(h.level_view(l).A.n_rows) for l in range(info.n_levels)]}
         g = P.GpuVcycle(h)
-        g.pcg(prob.rhs)
+        g.pcg(prob.rhs, max_it=args.max_it)
         ts = []
         for _ in range(3):
-            xg, rep = g.pcg(prob.rhs)
+            xg, rep = g.pcg(prob.rhs, max_it=args.max_it)
             ts.append(rep.T_s)
         rec.update({"gpu_n_it": rep.iterations, "gpu_converged": rep.converged, "gpu_T_s": min(ts),
                     "gpu_s_per_it": min(ts) / max(rep.iterations, 1), "gpu_true_rel_res": rep.true_rel_residual,
@@ -67,7 +69,7 @@ def main():
         if args.oracle:
             oh = O.OracleHierarchy(h, use_ref_spmv=O.ref_available(), threads=threads)
             t = time.perf_counter()
-            st, xo, ho, conv, trr = oh.pcg(prob.rhs)
+            st, xo, ho, conv, trr = oh.pcg(prob.rhs, max_it=args.max_it)
             t_cpu = time.perf_counter() - t
             k = min(20, rep.iterations, len(ho))
             rel_hist = float(np.max(np.abs(rep.residual_history[:k] - ho[:k]) / ho[:k])) if k else 0.0
@@ -80,7 +82,7 @@ def main():
                                    "pass": abs(rep.iterations - len(ho)) <= 1 and rel_hist <= 1e-9 and sol <= 1e-8}})
             print(cfg, "cpu", len(ho), round(t_cpu, 2), rec["parity"], flush=True)
         rec["wall_s"] = time.perf_counter() - t0
-        results[f"c{cfg}_s{args.scale}"] = rec
+        results[f"c{cfg}_s{args.scale}" + ("" if args.max_it == 1000 else f"_it{args.max_it}")] = rec
         g.close()
         del h
         os.makedirs(os.path.dirname(args.out), exist_ok=True)
