@@ -109,7 +109,7 @@ def get_hierarchy(P, cfg, scale, rank, dist, threads, setup_device=None):
     t0 = time.perf_counter()
     prob = P.Problem.config(cfg, scale)
     t_gen = time.perf_counter() - t0
-    cache_dir = os.path.join(ROOT, ".cache")
+    cache_dir = os.environ.get("ASPAMG_CACHE_DIR") or os.path.join(ROOT, ".cache")
     os.makedirs(cache_dir, exist_ok=True)
     key = f"hier_c{cfg}_s{scale}_{file_hash(os.path.join(N.LIB_DIR, 'libaspamg_host.so'))}.bin"
     path = os.path.join(cache_dir, key)

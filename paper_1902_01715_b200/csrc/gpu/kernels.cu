@@ -197,7 +197,7 @@ __device__ __forceinline__ void pdl_enter() {
 // a fixed shuffle tree (and, for T > 32, a fixed smem combine of the warp sums).
 constexpr int CSR_U = 4;
 
-template <int T, int STREAM, bool I16>
+template <int T, int STREAM, bool I16, int CSR_U = 4>
 __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* __restrict__ x, double* y,
                                                  const double* aux, double omega, const double* dotw, Red red,
                                                  const int* done) {
@@ -255,6 +255,181 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
             y[row] = out;
             if (dotw) dacc = fma(out, dotw[row], dacc);
         }
+    }
+    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
+}
+
+// ---------------------------------------------------- row-segment CSR SpMV
+// A warp owns 32 consecutive rows (lane l <-> row r0 + l). Their entries form
+// one contiguous CSR segment [rp[r0], rp[r0+32]); the warp streams it in tiles
+// of 32*U entries, lane l loading entries t0 + l + 32u (fully coalesced, no
+// padding, U value + U index loads then U x gathers in flight per lane), and
+// writes the products v*x (separately rounded multiply) to a per-warp shared
+// tile. Each lane then adds the products of its own row in ascending column
+// order — the reference spmv's sequential sum (sparse_matrix.cpp:100-105) with
+// separate multiply/add, so y is bit-identical to it regardless of row length
+// or how the segment splits into tiles.
+template <int U, int STREAM, bool I16, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_rseg(DCsr M, int epi, const double* __restrict__ x, double* y,
+                                                      const double* aux, double omega, const double* dotw, Red red,
+                                                      const int* done) {
+    pdl_enter();
+    if (is_done(done)) return;
+    constexpr int TILE = 32 * U;
+    __shared__ double prod[kBlock / 32][TILE];
+    const int lane = threadIdx.x & 31;
+    double* sp = prod[threadIdx.x >> 5];
+    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * kBlock) >> 5;
+    const int n = M.n_rows;
+    const int nblk = (n + 31) >> 5;
+    double dacc = 0.0;
+    for (int blk = warp; blk < nblk; blk += nwarps) {
+        const int row = blk * 32 + lane;
+        const bool act = row < n;
+        const int b = __ldg(M.rp + min(row, n));
+        int e = __shfl_down_sync(0xffffffffu, b, 1);
+        if (lane == 31) e = __ldg(M.rp + min(row + 1, n));
+        if (!act) e = b;
+        const int s0 = __shfl_sync(0xffffffffu, b, 0);
+        const int s1 = __shfl_sync(0xffffffffu, e, 31);
+        const double* xb = I16 ? x + __ldg(M.cb + blk) : x;
+        double s = 0.0;
+        int k = b;
+        for (int t0 = s0; t0 < s1; t0 += TILE) {
+            const int t1 = min(t0 + TILE, s1);
+            double v[U], xv[U];
+            int c[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int kk = t0 + lane + 32 * u;
+                v[u] = 0.0;
+                c[u] = 0;
+                if (kk < t1) {
+                    v[u] = ld_mat<STREAM>(M.v + kk);
+                    if constexpr (I16) c[u] = ld_mat<STREAM>(M.ci16 + kk);
+                    else c[u] = ld_mat<STREAM>(M.ci + kk);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) xv[u] = (t0 + lane + 32 * u < t1) ? __ldg(xb + c[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) sp[lane + 32 * u] = __dmul_rn(v[u], xv[u]);
+            __syncwarp();
+            const int ke = min(e, t1);
+            for (; k < ke; ++k) s = __dadd_rn(s, sp[k - t0]);
+            __syncwarp();
+        }
+        if (act) {
+            const double out = epilogue(epi, s, aux, row, omega);
+            y[row] = out;
+            if (dotw) dacc = fma(out, dotw[row], dacc);
+        }
+    }
+    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
+}
+
+// Pipelined row-segment kernel: same layout, tiles and arithmetic as k_rseg
+// (bit-identical results), but the matrix loads of the NEXT tile (of this
+// block, or the first tile of the warp's next block, whose row pointers are
+// fetched one block ahead) are issued before the current tile's products are
+// formed and summed, so each warp keeps two tiles of loads in flight and the
+// row-pointer / sum latencies hide behind them.
+template <int U, int STREAM, bool I16, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_rsegp(DCsr M, int epi, const double* __restrict__ x, double* y,
+                                                       const double* aux, double omega, const double* dotw, Red red,
+                                                       const int* done) {
+    pdl_enter();
+    if (is_done(done)) return;
+    constexpr int TILE = 32 * U;
+    __shared__ double prod[kBlock / 32][TILE];
+    const int lane = threadIdx.x & 31;
+    double* sp = prod[threadIdx.x >> 5];
+    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * kBlock) >> 5;
+    const int n = M.n_rows;
+    const int nblk = (n + 31) >> 5;
+    double dacc = 0.0;
+    // block state: own row extent [b, e), segment [s0, s1), 16-bit base
+    auto block_rows = [&](int blk, int& b, int& e, int& s0, int& s1, int& cb) {
+        const int row = blk * 32 + lane;
+        b = __ldg(M.rp + min(row, n));
+        e = __shfl_down_sync(0xffffffffu, b, 1);
+        if (lane == 31) e = __ldg(M.rp + min(row + 1, n));
+        if (row >= n) e = b;
+        s0 = __shfl_sync(0xffffffffu, b, 0);
+        s1 = __shfl_sync(0xffffffffu, e, 31);
+        cb = I16 ? __ldg(M.cb + blk) : 0;
+    };
+    double v[U];
+    int c[U];
+    auto load_tile = [&](int t0, int t1) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int kk = t0 + lane + 32 * u;
+            v[u] = 0.0;
+            c[u] = 0;
+            if (kk < t1) {
+                v[u] = ld_mat<STREAM>(M.v + kk);
+                if constexpr (I16) c[u] = ld_mat<STREAM>(M.ci16 + kk);
+                else c[u] = ld_mat<STREAM>(M.ci + kk);
+            }
+        }
+    };
+    int blk = warp;
+    if (blk >= nblk) {
+        if (red.fin != FIN_NONE) reduce_finish(dacc, red);
+        return;
+    }
+    int b, e, s0, s1, cb;
+    block_rows(blk, b, e, s0, s1, cb);
+    int t0 = s0;
+    load_tile(t0, min(t0 + TILE, s1));
+    double s = 0.0;
+    int k = b;
+    while (true) {
+        const int t1 = min(t0 + TILE, s1);
+        const bool last_tile = t0 + TILE >= s1;
+        // next tile coordinates (next block's row pointers fetched now)
+        int nb = blk, nb_b = b, nb_e = e, nb_s0 = s0, nb_s1 = s1, nb_cb = cb, nt0 = t0 + TILE;
+        if (last_tile) {
+            nb = blk + nwarps;
+            if (nb < nblk) {
+                block_rows(nb, nb_b, nb_e, nb_s0, nb_s1, nb_cb);
+                nt0 = nb_s0;
+            }
+        }
+        const double* xb = x + cb;
+        double xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = (t0 + lane + 32 * u < t1) ? __ldg(xb + c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = __dmul_rn(v[u], xv[u]);
+        if (nb < nblk) load_tile(nt0, min(nt0 + TILE, nb_s1));
+#pragma unroll
+        for (int u = 0; u < U; ++u) sp[lane + 32 * u] = xv[u];
+        __syncwarp();
+        const int ke = min(e, t1);
+        for (; k < ke; ++k) s = __dadd_rn(s, sp[k - t0]);
+        __syncwarp();
+        if (last_tile) {
+            const int row = blk * 32 + lane;
+            if (row < n) {
+                const double out = epilogue(epi, s, aux, row, omega);
+                y[row] = out;
+                if (dotw) dacc = fma(out, dotw[row], dacc);
+            }
+            if (nb >= nblk) break;
+            blk = nb;
+            b = nb_b;
+            e = nb_e;
+            s0 = nb_s0;
+            s1 = nb_s1;
+            cb = nb_cb;
+            s = 0.0;
+            k = b;
+        }
+        t0 = nt0;
     }
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
 }
@@ -909,7 +1084,16 @@ int occ_grid(K kern, long long work_units_per_cta_needed, size_t smem = 0) {
 #define SELLK(UU, P, MB)                                                                            \
     (M.sell.chh == 32 ? (M.sell.ci16 ? k_sell<UU, P, MB, true, 32> : k_sell<UU, P, MB, false, 32>)   \
                       : (M.sell.ci16 ? k_sell<UU, P, MB, true, 0> : k_sell<UU, P, MB, false, 0>))
-#define CSRK(GG, P) (M.csr.ci16 ? k_csr<GG, P, true> : k_csr<GG, P, false>)
+// csr_u = 8: eight loads per thread per round for long rows (T >= 32)
+#define CSRK(GG, P)                                                                                  \
+    (M.csr.u8 ? (M.csr.ci16 ? k_csr<GG, P, true, (GG >= 32 ? 8 : 4)> : k_csr<GG, P, false, (GG >= 32 ? 8 : 4)>) \
+              : (M.csr.ci16 ? k_csr<GG, P, true> : k_csr<GG, P, false>))
+#define RSEGK(UU, P, MB) (M.csr.ci16 ? k_rseg<UU, P, true, MB> : k_rseg<UU, P, false, MB>)
+#define RSEGPK(UU, P, MB) (M.csr.ci16 ? k_rsegp<UU, P, true, MB> : k_rsegp<UU, P, false, MB>)
+// Row-segment variants (U*10 + min CTAs/SM) instantiated below.
+#define ASPAMG_RSEG_VARIANTS(X) X(8, 4) X(8, 3) X(16, 2) X(4, 6)
+// Pipelined variants (rseg code 1000 + U*10 + min CTAs/SM).
+#define ASPAMG_RSEGP_VARIANTS(X) X(4, 4) X(4, 5) X(8, 2) X(8, 3)
 
 int spmv_grid(const DMat& M) {
     if (M.fmt == 1) {
@@ -946,6 +1130,24 @@ int spmv_grid(const DMat& M) {
         ASPAMG_SELL_OCC(4, 6)
         ASPAMG_SELL_OCC(2, 1)
 #undef ASPAMG_SELL_OCC
+        return 1;
+    }
+    if (M.csr.rseg) {
+        const long long wb = ((long long)M.csr.n_rows + 31) / 32;  // 32-row blocks, one per warp
+        const long long ctas = (wb + kBlock / 32 - 1) / (kBlock / 32);
+        const int st = M.csr.pol;
+#define ASPAMG_RSEG_OCC(UU, MB)                                                                   \
+    if (M.csr.rseg == UU * 10 + MB)                                                               \
+        return st == 1 ? occ_grid(RSEGK(UU, 1, MB), ctas)                                         \
+                       : st == 2 ? occ_grid(RSEGK(UU, 2, MB), ctas) : occ_grid(RSEGK(UU, 0, MB), ctas);
+        ASPAMG_RSEG_VARIANTS(ASPAMG_RSEG_OCC)
+#undef ASPAMG_RSEG_OCC
+#define ASPAMG_RSEGP_OCC(UU, MB)                                                                  \
+    if (M.csr.rseg == 1000 + UU * 10 + MB)                                                        \
+        return st == 1 ? occ_grid(RSEGPK(UU, 1, MB), ctas)                                        \
+                       : st == 2 ? occ_grid(RSEGPK(UU, 2, MB), ctas) : occ_grid(RSEGPK(UU, 0, MB), ctas);
+        ASPAMG_RSEGP_VARIANTS(ASPAMG_RSEGP_OCC)
+#undef ASPAMG_RSEGP_OCC
         return 1;
     }
     const int T = M.csr.group;
@@ -1018,6 +1220,33 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
         ASPAMG_SELL(4, 6)
         ASPAMG_SELL(2, 1)
 #undef ASPAMG_SELL
+        return;
+    }
+    if (M.csr.rseg) {
+#define ASPAMG_RSEG(UU, MB)                                                                                         \
+    if (M.csr.rseg == UU * 10 + MB) {                                                                              \
+        if (M.csr.pol == 1)                                                                                        \
+            launch(RSEGK(UU, 1, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
+        else if (M.csr.pol == 2)                                                                                   \
+            launch(RSEGK(UU, 2, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
+        else                                                                                                       \
+            launch(RSEGK(UU, 0, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
+        return;                                                                                                    \
+    }
+        ASPAMG_RSEG_VARIANTS(ASPAMG_RSEG)
+#undef ASPAMG_RSEG
+#define ASPAMG_RSEGP(UU, MB)                                                                                        \
+    if (M.csr.rseg == 1000 + UU * 10 + MB) {                                                                       \
+        if (M.csr.pol == 1)                                                                                        \
+            launch(RSEGPK(UU, 1, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);     \
+        else if (M.csr.pol == 2)                                                                                   \
+            launch(RSEGPK(UU, 2, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);     \
+        else                                                                                                       \
+            launch(RSEGPK(UU, 0, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);     \
+        return;                                                                                                    \
+    }
+        ASPAMG_RSEGP_VARIANTS(ASPAMG_RSEGP)
+#undef ASPAMG_RSEGP
         return;
     }
 #define ASPAMG_CSR_CASE(GG)                                                                                   \

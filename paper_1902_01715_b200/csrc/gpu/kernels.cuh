@@ -27,6 +27,14 @@ struct DCsr {
     // column = cb[row] + ci16[k] (10 instead of 12 matrix bytes per entry)
     unsigned short* ci16 = nullptr;
     int* cb = nullptr;
+    // Row-segment mode (k_rseg, 0 = off, else U*10 + min CTAs/SM): a warp owns 32
+    // consecutive rows, streams their contiguous CSR segment in tiles of 32*U
+    // entries (every lane loads consecutive entries: no padding, U independent
+    // loads per lane in flight), stages the products v*x in shared memory, and
+    // each lane then sums its own row in ascending column order. With 16-bit
+    // offsets cb holds one base column per 32-row block (not per row).
+    int rseg = 0;
+    int u8 = 0;  // k_csr with 8 loads per thread per round (T >= 32)
 };
 
 // Sliced 3x3-block format for an exactly 3x3-blocked operator (K): block

@@ -289,3 +289,25 @@ def test_sell_layout_variants_are_bit_identical(pkg, opts):
     if "pdl" in opts:
         g2 = _gpu(pkg, h, pdl=1, sell_chh=32, sell_sort_fill_pct=100000, sell_min_mean=1)  # restore the default
         assert np.array_equal(g2.apply(y), ref)
+
+
+@pytest.mark.parametrize("opts", [{}, {"rseg_u": 83}, {"rseg_u": 162}, {"rseg_u": 46}, {"idx16": 0},
+                                  {"rseg_u": 1044}, {"rseg_u": 1083}, {"rseg_u": 1082, "idx16": 0}])
+def test_rseg_spmv_bit_exact_every_operand(pkg, oracle, opts):
+    """Row-segment CSR kernel (k_rseg): products staged in shared memory, each
+    row summed sequentially in ascending column order with separate mul/add ->
+    bit-identical to the oracle's (= the reference's) spmv on every operand,
+    whatever the row length (rows longer than a tile span several tiles)."""
+    p, h = problem_and_hierarchy(2, 2)
+    g = _gpu(pkg, h, rseg=2, rseg_max_mean=100000, bsr=0, **opts)
+    o = _oracle(oracle, h)
+    rng = np.random.default_rng(11)
+    names = ["A", "G", "Gt", "P", "Pt"]
+    for l in range(h.n_levels):
+        for wi, which in enumerate(names):
+            if l == h.n_levels - 1 and which != "A":
+                continue
+            m = getattr(h.level(l, copy=False), which)
+            x = rng.standard_normal(m.n_cols)
+            assert np.array_equal(g.spmv(l, wi, x), o.spmv(l, which, x)), (opts, which, l)
+    _pcg_parity(p, h, g, o)
