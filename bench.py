@@ -118,6 +118,8 @@ def get_hierarchy(P, cfg, scale, rank, dist, threads, setup_device=None):
         t0 = time.perf_counter()
         h = P.Hierarchy.setup(prob.K, prob.coords, threads=threads, setup_device=setup_device)
         t_setup = time.perf_counter() - t0
+        if os.environ.get("ASPAMG_NO_CACHE"):  # single-process runs of huge configs: skip the dump
+            return prob, h, t_gen, t_setup
         h.save(path + ".tmp")
         os.replace(path + ".tmp", path)
     dist.barrier()

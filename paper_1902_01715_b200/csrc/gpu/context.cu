@@ -182,7 +182,8 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     }
     bool sell = v.n_rows >= c->opt_sell_min_rows && mean <= (double)c->opt_sell_max_mean &&
                 mean >= (double)c->opt_sell_min_mean && maxlen <= c->opt_sell_max_len;
-    const bool rseg = c->opt_rseg > 0 && v.n_rows > 0 && mean <= (double)c->opt_rseg_max_mean;
+    const bool rseg = c->opt_rseg > 0 && v.n_rows > 0 && v.n_rows >= c->opt_rseg_min_rows &&
+                      mean <= (double)c->opt_rseg_max_mean;
     if (rseg && c->opt_rseg >= 2) sell = false;
     if (sell && c->opt_sell_chh == 0 && !c->opt_sell_sort && nnz > 0) {
         // natural order only (sorted SELL loses the x-gather locality): fall back
@@ -809,6 +810,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "csr_u8") c->opt_csr_u8 = value;
         else if (k == "rseg_u") c->opt_rseg_u = value;
         else if (k == "rseg_max_mean") c->opt_rseg_max_mean = value;
+        else if (k == "rseg_min_rows") c->opt_rseg_min_rows = value;
         else if (k == "idx16_max_group") c->opt_idx16_max_group = value;
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;
         else if (k == "sell_max_len") c->opt_sell_max_len = value;

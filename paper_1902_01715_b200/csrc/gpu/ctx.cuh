@@ -67,7 +67,7 @@ struct aspamg_gpu_ctx {
     // row-segment CSR kernel (k_rseg): 0 off, 1 for CSR-format short-row operands,
     // 2 also instead of SELL; rseg_u = variant (U*10 + CTAs/SM, 0 = auto)
     long long opt_csr_u8 = 0;  // long-row CSR (T >= 32): 8 loads per thread per round
-    long long opt_rseg = 0, opt_rseg_u = 0, opt_rseg_max_mean = 64;
+    long long opt_rseg = 0, opt_rseg_u = 0, opt_rseg_max_mean = 64, opt_rseg_min_rows = 65536;
     long long opt_idx16 = 1;  // 16-bit column offsets where every row spans < 2^16 columns
     long long opt_idx16_max_group = 16;  // ... and (CSR) at most this many threads per row
     long long opt_stream_bytes = 48ll << 20, opt_keep_bytes = 64ll << 20, opt_tail_rows = 0, opt_csr_per_thread = 4;

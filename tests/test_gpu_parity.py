@@ -299,7 +299,7 @@ def test_rseg_spmv_bit_exact_every_operand(pkg, oracle, opts):
     bit-identical to the oracle's (= the reference's) spmv on every operand,
     whatever the row length (rows longer than a tile span several tiles)."""
     p, h = problem_and_hierarchy(2, 2)
-    g = _gpu(pkg, h, rseg=2, rseg_max_mean=100000, bsr=0, **opts)
+    g = _gpu(pkg, h, rseg=2, rseg_max_mean=100000, rseg_min_rows=0, bsr=0, **opts)
     o = _oracle(oracle, h)
     rng = np.random.default_rng(11)
     names = ["A", "G", "Gt", "P", "Pt"]

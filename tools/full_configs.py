@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--oracle", type=int, default=1, help="run the CPU oracle solve (0 = GPU only)")
     ap.add_argument("--max-it", type=int, default=1000,
                     help="PCG iteration cap (the paper's 1000, PAPER.md:1211; C4 needs more at full size)")
+    ap.add_argument("--gpu-reps", type=int, default=3, help="timed GPU solves (after one warm-up)")
     ap.add_argument("--gpu-setup", type=int, default=0, help="SRQCG + Galerkin on the GPU (bit-identical hierarchy)")
     args = ap.parse_args()
 
@@ -59,7 +60,7 @@ def main():
         g = P.GpuVcycle(h)
         g.pcg(prob.rhs, max_it=args.max_it)
         ts = []
-        for _ in range(3):
+        for _ in range(max(1, args.gpu_reps)):
             xg, rep = g.pcg(prob.rhs, max_it=args.max_it)
             ts.append(rep.T_s)
         rec.update({"gpu_n_it": rep.iterations, "gpu_converged": rep.converged, "gpu_T_s": min(ts),
