@@ -291,6 +291,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     A.group = group_for(mean, maxlen, v.n_rows, (double)c->opt_csr_per_thread);
     if (rseg) A.rseg = c->opt_rseg_u > 0 ? (int)c->opt_rseg_u : 84;
     A.u8 = (int)c->opt_csr_u8;
+    A.pf = (int)c->opt_csr_pf;
     // 16-bit offsets pay off for short rows (few threads per row, index bytes a
     // larger share of the per-thread stream); long-row operands (group >= 32)
     // measured slower with them (tools/tune_kernels.py, profiles/README.md).
@@ -808,6 +809,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "idx16") c->opt_idx16 = value;
         else if (k == "rseg") c->opt_rseg = value;
         else if (k == "csr_u8") c->opt_csr_u8 = value;
+        else if (k == "csr_pf") c->opt_csr_pf = value;
         else if (k == "rseg_u") c->opt_rseg_u = value;
         else if (k == "rseg_max_mean") c->opt_rseg_max_mean = value;
         else if (k == "rseg_min_rows") c->opt_rseg_min_rows = value;

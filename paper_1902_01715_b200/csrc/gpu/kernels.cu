@@ -197,7 +197,10 @@ __device__ __forceinline__ void pdl_enter() {
 // a fixed shuffle tree (and, for T > 32, a fixed smem combine of the warp sums).
 constexpr int CSR_U = 4;
 
-template <int T, int STREAM, bool I16, int CSR_U = 4>
+// PF: the row pointers (and 16-bit base) of the thread's NEXT row are loaded
+// one step ahead, so a step costs two dependent memory round trips (values,
+// then x) instead of three.
+template <int T, int STREAM, bool I16, int CSR_U = 4, bool PF = false>
 __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* __restrict__ x, double* y,
                                                  const double* aux, double omega, const double* dotw, Red red,
                                                  const int* done) {
@@ -208,13 +211,39 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
     const int t = threadIdx.x % T;
     const int lr = threadIdx.x / T;
     const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * RPC;
     double dacc = 0.0;
-    for (int rbase = blockIdx.x * RPC; rbase < M.n_rows; rbase += gridDim.x * RPC) {
+    int pb = 0, pe = 0, pc = 0;
+    if constexpr (PF) {
+        const int row = blockIdx.x * RPC + lr;
+        if (row < M.n_rows) {
+            pb = __ldg(M.rp + row);
+            pe = __ldg(M.rp + row + 1);
+            if constexpr (I16) pc = __ldg(M.cb + row);
+        }
+    }
+    for (int rbase = blockIdx.x * RPC; rbase < M.n_rows; rbase += stride) {
         const int row = rbase + lr;
         double s = 0.0;
+        int b, e, cbase;
+        if constexpr (PF) {
+            b = pb;
+            e = pe;
+            cbase = pc;
+            const int nrow = row + stride;
+            if (nrow < M.n_rows) {
+                pb = __ldg(M.rp + nrow);
+                pe = __ldg(M.rp + nrow + 1);
+                if constexpr (I16) pc = __ldg(M.cb + nrow);
+            }
+        }
         if (row < M.n_rows) {
-            const int b = __ldg(M.rp + row), e = __ldg(M.rp + row + 1);
-            const double* xr = I16 ? x + __ldg(M.cb + row) : x;
+            if constexpr (!PF) {
+                b = __ldg(M.rp + row);
+                e = __ldg(M.rp + row + 1);
+                cbase = I16 ? __ldg(M.cb + row) : 0;
+            }
+            const double* xr = I16 ? x + cbase : x;
             for (int k0 = b + t; k0 < e; k0 += T * CSR_U) {
                 double v[CSR_U], xv[CSR_U];
                 int c[CSR_U];
@@ -1084,10 +1113,22 @@ int occ_grid(K kern, long long work_units_per_cta_needed, size_t smem = 0) {
 #define SELLK(UU, P, MB)                                                                            \
     (M.sell.chh == 32 ? (M.sell.ci16 ? k_sell<UU, P, MB, true, 32> : k_sell<UU, P, MB, false, 32>)   \
                       : (M.sell.ci16 ? k_sell<UU, P, MB, true, 0> : k_sell<UU, P, MB, false, 0>))
-// csr_u = 8: eight loads per thread per round for long rows (T >= 32)
-#define CSRK(GG, P)                                                                                  \
-    (M.csr.u8 ? (M.csr.ci16 ? k_csr<GG, P, true, (GG >= 32 ? 8 : 4)> : k_csr<GG, P, false, (GG >= 32 ? 8 : 4)>) \
-              : (M.csr.ci16 ? k_csr<GG, P, true> : k_csr<GG, P, false>))
+// CSR kernel variant of an operand: u8 = 1 eight loads per thread per round for
+// long rows (T >= 32), u8 = 2 for every T; pf = row-pointer prefetch (T <= 16).
+using SpmvKern = void (*)(DCsr, int, const double*, double*, const double*, double, const double*, Red, const int*);
+template <int GG, int P, bool I16>
+SpmvKern csr_kernel_i(const DCsr& A) {
+    const bool u8 = A.u8 == 2 || (A.u8 == 1 && GG >= 32);
+    if constexpr (GG <= 16) {
+        if (A.pf) return u8 ? k_csr<GG, P, I16, 8, true> : k_csr<GG, P, I16, 4, true>;
+    }
+    return u8 ? k_csr<GG, P, I16, 8> : k_csr<GG, P, I16, 4>;
+}
+template <int GG, int P>
+SpmvKern csr_kernel(const DCsr& A) {
+    return A.ci16 ? csr_kernel_i<GG, P, true>(A) : csr_kernel_i<GG, P, false>(A);
+}
+#define CSRK(GG, P) csr_kernel<GG, P>(M.csr)
 #define RSEGK(UU, P, MB) (M.csr.ci16 ? k_rseg<UU, P, true, MB> : k_rseg<UU, P, false, MB>)
 #define RSEGPK(UU, P, MB) (M.csr.ci16 ? k_rsegp<UU, P, true, MB> : k_rsegp<UU, P, false, MB>)
 // Row-segment variants (U*10 + min CTAs/SM) instantiated below.

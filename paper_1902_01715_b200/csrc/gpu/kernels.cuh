@@ -34,7 +34,8 @@ struct DCsr {
     // each lane then sums its own row in ascending column order. With 16-bit
     // offsets cb holds one base column per 32-row block (not per row).
     int rseg = 0;
-    int u8 = 0;  // k_csr with 8 loads per thread per round (T >= 32)
+    int u8 = 0;  // k_csr with 8 loads per thread per round (1: T >= 32, 2: every T)
+    int pf = 0;  // k_csr row-pointer prefetch (T <= 16)
 };
 
 // Sliced 3x3-block format for an exactly 3x3-blocked operator (K): block

@@ -311,3 +311,15 @@ def test_rseg_spmv_bit_exact_every_operand(pkg, oracle, opts):
             x = rng.standard_normal(m.n_cols)
             assert np.array_equal(g.spmv(l, wi, x), o.spmv(l, which, x)), (opts, which, l)
     _pcg_parity(p, h, g, o)
+
+
+@pytest.mark.parametrize("opts", [{"csr_u8": 1}, {"csr_u8": 2}, {"csr_pf": 1}, {"csr_u8": 2, "csr_pf": 1},
+                                  {"csr_pf": 1, "idx16": 0}])
+def test_csr_kernel_variants_are_bit_identical(pkg, opts):
+    """CSR kernel variants (8 loads per round, row-pointer prefetch) keep every
+    thread's entries and their order, so the V-cycle output is bit-identical."""
+    p, h = problem_and_hierarchy(2, 2)
+    y = np.random.default_rng(9).standard_normal(p.K.n_rows)
+    base = {"idx16": 0} if opts.get("idx16") == 0 else {}
+    ref = _gpu(pkg, h, **base).apply(y)
+    assert np.array_equal(_gpu(pkg, h, **opts).apply(y), ref)
