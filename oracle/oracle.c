@@ -35,7 +35,25 @@ int orc_spmv(const orc_csr* A, const double* x, double* y) {
     return 0;
 }
 
+/* dot_mode 0 (default): one sequential sum in index order (the reference's
+ * single-thread order). dot_mode 1: 4096-element blocks summed sequentially,
+ * block partials summed in index order — an equally valid fixed order, used
+ * only to measure how sensitive a solve's iteration count is to the dot's
+ * summation order. */
+static int g_dot_mode = 0;
+void orc_set_dot_mode(int m) { g_dot_mode = m; }
+
 static double dotp(int64_t n, const double* a, const double* b) {
+    if (g_dot_mode == 1) {
+        double s = 0.0;
+        for (int64_t i0 = 0; i0 < n; i0 += 4096) {
+            const int64_t i1 = i0 + 4096 < n ? i0 + 4096 : n;
+            double t = 0.0;
+            for (int64_t i = i0; i < i1; ++i) t += a[i] * b[i];
+            s += t;
+        }
+        return s;
+    }
     double s = 0.0;
     for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
     return s;

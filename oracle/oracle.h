@@ -55,6 +55,7 @@ typedef struct orc_hier {
 typedef void (*orc_spmv_hook)(void* ref, const double* x, double* y);
 
 void orc_set_threads(int n);
+void orc_set_dot_mode(int mode); /* 0 sequential (default); 1 blocked (sensitivity studies only) */
 void orc_set_spmv_hook(orc_spmv_hook fn); /* NULL = the oracle's own loop */
 
 int orc_spmv(const orc_csr* A, const double* x, double* y);

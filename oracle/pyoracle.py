@@ -46,6 +46,7 @@ def lib() -> C.CDLL:
     if _lib is None:
         _lib = C.CDLL(os.path.join(HERE, "liboracle.so"))
         _lib.orc_set_threads.argtypes = [C.c_int]
+        _lib.orc_set_dot_mode.argtypes = [C.c_int]
         _lib.orc_set_spmv_hook.argtypes = [C.c_void_p]
         _lib.orc_spmv.argtypes = [C.POINTER(OrcCsr), P_dbl, P_dbl]
         _lib.orc_smooth.argtypes = [C.POINTER(OrcHier), i64, P_dbl, P_dbl, P_dbl]

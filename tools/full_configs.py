@@ -75,6 +75,9 @@ def main():
             k = min(20, rep.iterations, len(ho))
             rel_hist = float(np.max(np.abs(rep.residual_history[:k] - ho[:k]) / ho[:k])) if k else 0.0
             sol = float(np.linalg.norm(xg - xo) / np.linalg.norm(xo))
+            hg = np.asarray(rep.residual_history)
+            rec["history"] = {"every": 50, "gpu": hg[::50].tolist(), "cpu": np.asarray(ho)[::50].tolist(),
+                              "gpu_tail": hg[-12:].tolist(), "cpu_tail": np.asarray(ho)[-12:].tolist()}
             rec.update({"cpu_n_it": len(ho), "cpu_converged": conv, "cpu_T_s": t_cpu,
                         "cpu_s_per_it": t_cpu / max(len(ho), 1), "cpu_threads": threads,
                         "cpu_kind": "reference spmv (oracle/_ref)" if O.ref_available() else "oracle port",
