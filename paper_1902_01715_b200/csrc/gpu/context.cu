@@ -292,6 +292,19 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     if (rseg) A.rseg = c->opt_rseg_u > 0 ? (int)c->opt_rseg_u : 84;
     A.u8 = (int)c->opt_csr_u8;
     A.pf = (int)c->opt_csr_pf;
+    if (c->opt_csr_long > 0 && !rseg && A.group <= 16) {
+        const int thr = (int)c->opt_csr_long * A.group * 4;
+        std::vector<int> lr;
+        for (int64_t i = 0; i < v.n_rows; ++i)
+            if (len[(size_t)i] > thr) lr.push_back((int)i);
+        if (!lr.empty()) {
+            A.nlong = (int)lr.size();
+            A.lthr = thr;
+            A.nlctas = (int)std::min<int64_t>((lr.size() + kBlock / 32 - 1) / (kBlock / 32), 296);
+            A.lrows = dalloc<int>(c, lr.size());
+            CK(cudaMemcpy(A.lrows, lr.data(), lr.size() * sizeof(int), cudaMemcpyHostToDevice));
+        }
+    }
     // 16-bit offsets pay off for short rows (few threads per row, index bytes a
     // larger share of the per-thread stream); long-row operands (group >= 32)
     // measured slower with them (tools/tune_kernels.py, profiles/README.md).
@@ -398,7 +411,7 @@ void add_spmv(aspamg_gpu_ctx* c, std::vector<Op>& ops, const std::string& name, 
                        Launch L{grid, s};
                        spmv(Mc, epi, x, y, aux, omega, dotw, red, done, L);
                    }});
-    if (M.fmt == 0 && !M.csr.rseg && fin == FIN_NONE && !dotw) {
+    if (M.fmt == 0 && !M.csr.rseg && !M.csr.nlong && fin == FIN_NONE && !dotw) {
         Op& o = ops.back();
         o.describable = true;
         o.desc.kind = 0;
@@ -810,6 +823,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "rseg") c->opt_rseg = value;
         else if (k == "csr_u8") c->opt_csr_u8 = value;
         else if (k == "csr_pf") c->opt_csr_pf = value;
+        else if (k == "csr_long") c->opt_csr_long = value;
         else if (k == "rseg_u") c->opt_rseg_u = value;
         else if (k == "rseg_max_mean") c->opt_rseg_max_mean = value;
         else if (k == "rseg_min_rows") c->opt_rseg_min_rows = value;

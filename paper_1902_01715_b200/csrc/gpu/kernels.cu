@@ -211,21 +211,61 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
     const int t = threadIdx.x % T;
     const int lr = threadIdx.x / T;
     const int lane = threadIdx.x & 31;
-    const int stride = gridDim.x * RPC;
     double dacc = 0.0;
+    if ((int)blockIdx.x < M.nlctas) {
+        // Long-row CTAs: one warp per row of the long-row list (rows longer than
+        // lthr), 32 lanes x CSR_U loads per round, fixed shuffle tree.
+        const int nw = M.nlctas * (kBlock / 32);
+        for (int q = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); q < M.nlong; q += nw) {
+            const int row = __ldg(M.lrows + q);
+            const int b = __ldg(M.rp + row), e = __ldg(M.rp + row + 1);
+            const double* xr = I16 ? x + __ldg(M.cb + row) : x;
+            double s = 0.0;
+            for (int k0 = b + lane; k0 < e; k0 += 32 * CSR_U) {
+                double v[CSR_U], xv[CSR_U];
+                int c[CSR_U];
+#pragma unroll
+                for (int u = 0; u < CSR_U; ++u) {
+                    const int k = k0 + u * 32;
+                    v[u] = 0.0;
+                    c[u] = 0;
+                    if (k < e) {
+                        v[u] = ld_mat<STREAM>(M.v + k);
+                        if constexpr (I16) c[u] = ld_mat<STREAM>(M.ci16 + k);
+                        else c[u] = ld_mat<STREAM>(M.ci + k);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < CSR_U; ++u) xv[u] = (k0 + u * 32 < e) ? __ldg(xr + c[u]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < CSR_U; ++u) s = fma(v[u], xv[u], s);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+            if (lane == 0) {
+                const double out = epilogue(epi, s, aux, row, omega);
+                y[row] = out;
+                if (dotw) dacc = fma(out, dotw[row], dacc);
+            }
+        }
+        if (red.fin != FIN_NONE) reduce_finish(dacc, red);
+        return;
+    }
+    const int bid = (int)blockIdx.x - M.nlctas;
+    const int stride = ((int)gridDim.x - M.nlctas) * RPC;
     int pb = 0, pe = 0, pc = 0;
     if constexpr (PF) {
-        const int row = blockIdx.x * RPC + lr;
+        const int row = bid * RPC + lr;
         if (row < M.n_rows) {
             pb = __ldg(M.rp + row);
             pe = __ldg(M.rp + row + 1);
             if constexpr (I16) pc = __ldg(M.cb + row);
         }
     }
-    for (int rbase = blockIdx.x * RPC; rbase < M.n_rows; rbase += stride) {
+    for (int rbase = bid * RPC; rbase < M.n_rows; rbase += stride) {
         const int row = rbase + lr;
         double s = 0.0;
-        int b, e, cbase;
+        int b = 0, e = 0, cbase = 0;
         if constexpr (PF) {
             b = pb;
             e = pe;
@@ -236,13 +276,14 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
                 pe = __ldg(M.rp + nrow + 1);
                 if constexpr (I16) pc = __ldg(M.cb + nrow);
             }
+        } else if (row < M.n_rows) {
+            b = __ldg(M.rp + row);
+            e = __ldg(M.rp + row + 1);
+            cbase = I16 ? __ldg(M.cb + row) : 0;
         }
-        if (row < M.n_rows) {
-            if constexpr (!PF) {
-                b = __ldg(M.rp + row);
-                e = __ldg(M.rp + row + 1);
-                cbase = I16 ? __ldg(M.cb + row) : 0;
-            }
+        // rows on the long-row list are computed (and written) by the long-row CTAs
+        const bool own = row < M.n_rows && (M.nlong == 0 || e - b <= M.lthr);
+        if (own) {
             const double* xr = I16 ? x + cbase : x;
             for (int k0 = b + t; k0 < e; k0 += T * CSR_U) {
                 double v[CSR_U], xv[CSR_U];
@@ -279,7 +320,7 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
             }
             __syncthreads();
         }
-        if (t == 0 && row < M.n_rows) {
+        if (t == 0 && own) {
             const double out = epilogue(epi, s, aux, row, omega);
             y[row] = out;
             if (dotw) dacc = fma(out, dotw[row], dacc);
@@ -1194,8 +1235,10 @@ int spmv_grid(const DMat& M) {
     const int T = M.csr.group;
     const long long ctas = ((long long)M.csr.n_rows * T + kBlock - 1) / kBlock;
     const int st = M.csr.pol;
-#define ASPAMG_CSR_OCC(TT) \
-    case TT: return st == 1 ? occ_grid(CSRK(TT, 1), ctas) : st == 2 ? occ_grid(CSRK(TT, 2), ctas) : occ_grid(CSRK(TT, 0), ctas);
+    // + the long-row CTAs (M.csr.nlctas, fixed at upload) ahead of the regular grid
+#define ASPAMG_CSR_OCC(TT)                                                                                   \
+    case TT: return M.csr.nlctas + (st == 1 ? occ_grid(CSRK(TT, 1), ctas)                                    \
+                                            : st == 2 ? occ_grid(CSRK(TT, 2), ctas) : occ_grid(CSRK(TT, 0), ctas));
     switch (T) {
         ASPAMG_CSR_OCC(1)
         ASPAMG_CSR_OCC(2)

@@ -36,6 +36,12 @@ struct DCsr {
     int rseg = 0;
     int u8 = 0;  // k_csr with 8 loads per thread per round (1: T >= 32, 2: every T)
     int pf = 0;  // k_csr row-pointer prefetch (T <= 16)
+    // Long-row split: rows longer than lthr (listed in lrows) are computed by the
+    // first nlctas CTAs of the launch, one warp per row; the regular T-thread
+    // groups skip them, so a long-tailed operand (G' rows up to ~7x the mean) no
+    // longer waits on a few long serial chains.
+    int nlong = 0, lthr = 0, nlctas = 0;
+    int* lrows = nullptr;
 };
 
 // Sliced 3x3-block format for an exactly 3x3-blocked operator (K): block

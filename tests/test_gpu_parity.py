@@ -323,3 +323,26 @@ def test_csr_kernel_variants_are_bit_identical(pkg, opts):
     base = {"idx16": 0} if opts.get("idx16") == 0 else {}
     ref = _gpu(pkg, h, **base).apply(y)
     assert np.array_equal(_gpu(pkg, h, **opts).apply(y), ref)
+
+
+@pytest.mark.parametrize("opts", [{"csr_long": 1}, {"csr_long": 2}, {"csr_long": 4, "csr_pf": 0},
+                                  {"csr_long": 1, "idx16": 0}])
+def test_csr_long_row_split_matches_oracle(pkg, oracle, opts):
+    """Long-row split (rows past the threshold computed warp-per-row by extra
+    CTAs of the same launch): every operand within the CSR per-row bound, PCG
+    within the north_star tolerances, deterministic run to run."""
+    p, h = problem_and_hierarchy(2, 2)
+    g = _gpu(pkg, h, **opts)
+    o = _oracle(oracle, h)
+    rng = np.random.default_rng(13)
+    for l in range(h.n_levels - 1):
+        for wi, which in enumerate(["A", "G", "Gt", "P", "Pt"]):
+            m = getattr(h.level(l, copy=False), which)
+            x = rng.standard_normal(m.n_cols)
+            yg, yo = g.spmv(l, wi, x), o.spmv(l, which, x)
+            absrow = np.abs(m.to_scipy()) @ np.abs(x)
+            assert np.all(np.abs(yg - yo) <= 1e-14 * absrow + 1e-300), (opts, which, l)
+    y = rng.standard_normal(p.K.n_rows)
+    assert np.array_equal(g.apply(y), g.apply(y))
+    assert rel_err(g.apply(y), o.vcycle(y)) < RTOL_VCYCLE
+    _pcg_parity(p, h, g, o)
