@@ -65,8 +65,21 @@ const char* aspamg_gpu_last_error(const aspamg_gpu_ctx* ctx); /* ctx may be NULL
 int aspamg_gpu_device_count(int* n);
 int aspamg_gpu_ctx_create(int device, aspamg_gpu_ctx** out);
 int aspamg_gpu_ctx_destroy(aspamg_gpu_ctx* ctx);
-/* keys: "bsr" (1 auto, 0 never), "device_loop" (1 CUDA-graph while-loop, 0 host loop),
- *       "stream_bytes" (matrices above this many bytes use evict-first loads) */
+/* keys (set before the first upload; unknown keys -> status 4):
+ *   "bsr"          1 auto (exactly 3x3-blocked operands -> sliced BSR3), 0 never
+ *   "device_loop"  1 CUDA-graph while-loop (default), 0 host loop
+ *   "stream_bytes" operators above this many bytes use evict-first loads
+ *   "keep_bytes"   coarsest levels up to this many bytes load with evict-last
+ *   "coarse_mode"  1 explicit inverse-factor triangles (default), 0 one-CTA substitution
+ *   "idx16"        16-bit column offsets where rows span < 2^16 columns (default 1)
+ *   "sell_*"       SELL layout / kernel choices (chunk height, sorting window, unroll, TMA ring)
+ *   "csr_per_thread", "csr_u8", "csr_pf", "csr_long"  CSR kernel group size, loads per round,
+ *                  row-pointer prefetch (default on), long-row split threshold (0 = off)
+ *   "rseg", "rseg_u", "rseg_max_mean", "rseg_min_rows"  row-segment kernel (off by default)
+ *   "tail_rows"    levels below this many rows run as one persistent cooperative kernel (0 = off)
+ *   "pdl"          programmatic dependent launch (default 1)
+ * Every variant sums in a fixed order (deterministic); sliced / row-segment
+ * formats are bit-identical to the reference spmv (tests/test_gpu_parity.py). */
 int aspamg_gpu_set_option(aspamg_gpu_ctx* ctx, const char* key, int64_t value);
 int aspamg_gpu_set_cycle(aspamg_gpu_ctx* ctx, int64_t nu1, int64_t nu2);
 /* Levels 0..L-2 carry A, G, G', P, P' and omega; the coarsest level L-1 carries

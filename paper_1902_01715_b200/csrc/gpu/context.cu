@@ -457,6 +457,10 @@ void build_vcycle(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* 
     const int L = (int)c->lv.size();
     const bool top = k == 0;
     if (allow_tail && k >= 1 && c->lv[(size_t)k].n <= c->opt_tail_rows && build_tail(c, ops, k, y, z, done)) return;
+    if (allow_tail && k >= 1 && k == c->tail_level) {  // collapsed coarse tail: z = T y
+        add_spmv(c, ops, "tail_dense", k, c->Tm, EPI_PLAIN, y, z, nullptr, 1.0, nullptr, FIN_NONE, nullptr, done);
+        return;
+    }
     if (k == L - 1) {  // coarsest: forward/backward solve
         Red red;
         const int n = c->n_c;
@@ -578,6 +582,53 @@ void build_device_loop(aspamg_gpu_ctx* c) {
     CK(cudaGraphInstantiate(&c->pcg_exec, c->pcg_graph, 0));
 }
 
+// Collapsed coarse tail: B_k, the V-cycle restricted to levels k..L-1, is a
+// fixed linear map (SPEC.md:445-453 with fixed G, P, omega and coarse factor).
+// Its matrix is formed on the device column by column — the sub-cycle's own
+// kernels applied to the unit vectors e_j — and stored as a dense CSR operand,
+// so the whole tail becomes one L2-resident product per V-cycle. Exact up to
+// rounding (different summation order), checked by the V-cycle/PCG parity tests.
+void build_dense_tail(aspamg_gpu_ctx* c) {
+    const int L = (int)c->lv.size();
+    int k = -1;
+    for (int q = 1; q < L; ++q)
+        if (c->lv[(size_t)q].n <= c->opt_tail_dense) { k = q; break; }
+    if (k < 0 || k == L - 1) return;  // nothing to collapse (the coarsest alone is already one solve)
+    const int n = c->lv[(size_t)k].n;
+    double* y = c->lv[(size_t)k].y;
+    double* z = c->lv[(size_t)k].z;
+    std::vector<Op> sub;
+    build_vcycle(c, sub, k, y, z, nullptr, FIN_NONE, nullptr, false);
+    double* dM = dalloc<double>(c, (size_t)n * n);
+    const double one = 1.0;
+    for (int j = 0; j < n; ++j) {
+        CK(cudaMemsetAsync(y, 0, (size_t)n * sizeof(double), c->stream));
+        CK(cudaMemcpyAsync(y + j, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        run_ops(sub, c->stream);
+        // column j of the row-major matrix: M[i][j] = z_i
+        CK(cudaMemcpy2DAsync(dM + j, (size_t)n * sizeof(double), z, sizeof(double), sizeof(double), (size_t)n,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CK(cudaGetLastError());
+    std::vector<double> M((size_t)n * n);
+    CK(cudaMemcpyAsync(M.data(), dM, M.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<int64_t> rp((size_t)n + 1), ci((size_t)n * n);
+    for (int i = 0; i <= n; ++i) rp[(size_t)i] = (int64_t)i * n;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) ci[(size_t)i * n + j] = j;
+    aspamg_csr_view v{};
+    v.n_rows = n;
+    v.n_cols = n;
+    v.nnz = (int64_t)n * n;
+    v.row_offsets = rp.data();
+    v.col_indices = ci.data();
+    v.values = M.data();
+    c->Tm = upload_mat(c, v, false);
+    set_pol(c->Tm, 2);
+    c->tail_level = k;
+}
+
 void do_finalize(aspamg_gpu_ctx* c) {
     if ((int)c->lv.size() < 1) throw Fail{4, "finalize: no levels uploaded"};
     if (!c->coarse_uploaded) throw Fail{4, "finalize: coarse factor not uploaded"};
@@ -632,6 +683,7 @@ void do_finalize(aspamg_gpu_ctx* c) {
                 if (i == 0 || l.has_smoother) set_pol(*ms[i], 2);
         }
     }
+    if (c->opt_tail_dense > 0) build_dense_tail(c);
     const int* done = &c->st->done;
     // standalone V-cycle: vy -> vz
     build_vcycle(c, c->vc_ops, 0, c->vy, c->vz, nullptr, FIN_NONE, c->zero_flag);
@@ -824,6 +876,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "csr_u8") c->opt_csr_u8 = value;
         else if (k == "csr_pf") c->opt_csr_pf = value;
         else if (k == "csr_long") c->opt_csr_long = value;
+        else if (k == "tail_dense") c->opt_tail_dense = value;
         else if (k == "rseg_u") c->opt_rseg_u = value;
         else if (k == "rseg_max_mean") c->opt_rseg_max_mean = value;
         else if (k == "rseg_min_rows") c->opt_rseg_min_rows = value;

@@ -57,6 +57,11 @@ struct aspamg_gpu_ctx {
     double *Lrm = nullptr, *Lcm = nullptr, *Dinv_f = nullptr, *Dinv_b = nullptr;
     double* cw = nullptr;  // temp between the two triangular products
     DMat Wm, Wtm;          // W = L^{-1} (lower) and W' (upper) as CSR operands
+    // Collapsed coarse tail (opt "tail_dense"): the V-cycle from level tail_level
+    // down is a fixed linear operator; its n x n matrix (columns = the sub-cycle
+    // applied to unit vectors on the device at finalize) replaces those levels.
+    int tail_level = -1;
+    DMat Tm;
     bool coarse_uploaded = false;
     bool finalized = false;
     // options
@@ -67,6 +72,7 @@ struct aspamg_gpu_ctx {
     // row-segment CSR kernel (k_rseg): 0 off, 1 for CSR-format short-row operands,
     // 2 also instead of SELL; rseg_u = variant (U*10 + CTAs/SM, 0 = auto)
     long long opt_csr_u8 = 0;  // CSR: 8 loads per thread per round (1: T >= 32, 2: every T)
+    long long opt_tail_dense = 0;  // collapse the V-cycle below the first level with <= this many rows (0 = off)
     long long opt_csr_long = 0;  // long-row split threshold in rounds (rows > long*T*4 entries; 0 = off)
     long long opt_csr_pf = 1;  // CSR (T <= 16): prefetch the next row's pointers (measured 1.4% faster per PCG iteration on C2)
     long long opt_rseg = 0, opt_rseg_u = 0, opt_rseg_max_mean = 64, opt_rseg_min_rows = 65536;

@@ -346,3 +346,18 @@ def test_csr_long_row_split_matches_oracle(pkg, oracle, opts):
     assert np.array_equal(g.apply(y), g.apply(y))
     assert rel_err(g.apply(y), o.vcycle(y)) < RTOL_VCYCLE
     _pcg_parity(p, h, g, o)
+
+
+@pytest.mark.parametrize("rows", [300, 2000, 8000])
+def test_dense_coarse_tail_matches_oracle(pkg, oracle, rows):
+    """Collapsed coarse tail (tail_dense): the V-cycle below the first level
+    with <= rows rows replaced by its own matrix, formed on the device from the
+    sub-cycle's kernels. Same operator up to rounding: V-cycle within 1e-11,
+    PCG within the north_star tolerances."""
+    p, h = problem_and_hierarchy(2, 2)
+    g = _gpu(pkg, h, tail_dense=rows)
+    o = _oracle(oracle, h)
+    y = np.random.default_rng(17).standard_normal(p.K.n_rows)
+    assert rel_err(g.apply(y), o.vcycle(y)) < RTOL_VCYCLE
+    assert np.array_equal(g.apply(y), g.apply(y))
+    _pcg_parity(p, h, g, o)
