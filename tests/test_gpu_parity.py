@@ -263,11 +263,11 @@ def test_one_level_hierarchy_is_direct_solve(pkg, oracle):
 def test_coarse_tail_persistent_kernel_matches_oracle(pkg, oracle, tail_rows):
     """Levels below tail_rows run as one persistent cooperative kernel; same results."""
     p, h = problem_and_hierarchy(1, 1)
-    g = _gpu(pkg, h, tail_rows=tail_rows)
+    g = _gpu(pkg, h, tail_rows=tail_rows, tail_dense=0)
     o = _oracle(oracle, h)
     y = np.random.default_rng(21).standard_normal(p.K.n_rows)
     assert rel_err(g.apply(y), o.vcycle(y)) < RTOL_VCYCLE
-    ref = _gpu(pkg, h)
+    ref = _gpu(pkg, h, tail_dense=0)
     assert np.array_equal(g.apply(y), ref.apply(y))  # same kernels' arithmetic, same bits
     _pcg_parity(p, h, g, o)
 
@@ -348,7 +348,7 @@ def test_csr_long_row_split_matches_oracle(pkg, oracle, opts):
     _pcg_parity(p, h, g, o)
 
 
-@pytest.mark.parametrize("rows", [300, 2000, 8000])
+@pytest.mark.parametrize("rows", [0, 300, 2000, 8000])
 def test_dense_coarse_tail_matches_oracle(pkg, oracle, rows):
     """Collapsed coarse tail (tail_dense): the V-cycle below the first level
     with <= rows rows replaced by its own matrix, formed on the device from the
