@@ -395,6 +395,8 @@ def run_b200(args, ws, rank, local):
                    "rel_tol": args.tol, "K_format": "bsr3" if lv0.a_format == 1 else "csr",
                    "setup_s": t_setup, "setup_on": "cpu" if args.cpu_setup else "cpu + gpu (srqcg, galerkin)",
                    "upload_s": t_upload, "parallelism": f"replicas x{ws}",
+                   "vcycle": "V(1,1), levels below the first with <= 1500 rows collapsed into one dense operator "
+                             "formed on the device at upload (tail_dense); CSR long rows split to warp-per-row CTAs",
                    "l2": "inputs larger than L2 (K alone > 126 MB), no flush" if args.config != 1 else "K fits in L2"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": top[0], "level": top[1], "kernel_ms": k_ms,
