@@ -292,7 +292,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     if (rseg) A.rseg = c->opt_rseg_u > 0 ? (int)c->opt_rseg_u : 84;
     A.u8 = (int)c->opt_csr_u8;
     A.pf = (int)c->opt_csr_pf;
-    if (c->opt_csr_long > 0 && !rseg && A.group <= 16) {
+    if (c->opt_csr_long > 0 && !rseg && A.group <= 16 && !(c->opt_csr_vec && A.group >= 16)) {
         const int thr = (int)c->opt_csr_long * A.group * 4;
         std::vector<int> lr;
         for (int64_t i = 0; i < v.n_rows; ++i)
@@ -309,7 +309,9 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     // larger share of the per-thread stream); long-row operands (group >= 32)
     // measured slower with them (tools/tune_kernels.py, profiles/README.md).
     // Row-segment mode: one base column per 32-row block.
-    const bool i16 = c->opt_idx16 && (rseg ? blocks_fit_u16(v) : A.group <= c->opt_idx16_max_group && rows_fit_u16(v));
+    const bool vec = c->opt_csr_vec && !rseg && A.group >= 16;
+    const bool i16 = c->opt_idx16 && (rseg ? blocks_fit_u16(v) : (vec || A.group <= c->opt_idx16_max_group) && rows_fit_u16(v));
+    A.vec = vec && i16;
     const int64_t nbase = rseg ? (v.n_rows + 31) / 32 : v.n_rows;
     std::vector<int> rp((size_t)v.n_rows + 1), ci(i16 ? 0 : (size_t)nnz), cb(i16 ? (size_t)std::max<int64_t>(nbase, 1) : 0);
     std::vector<unsigned short> c16(i16 ? (size_t)nnz : 0);
@@ -876,6 +878,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "csr_u8") c->opt_csr_u8 = value;
         else if (k == "csr_pf") c->opt_csr_pf = value;
         else if (k == "csr_long") c->opt_csr_long = value;
+        else if (k == "csr_vec") c->opt_csr_vec = value;
         else if (k == "tail_dense") c->opt_tail_dense = value;
         else if (k == "rseg_u") c->opt_rseg_u = value;
         else if (k == "rseg_max_mean") c->opt_rseg_max_mean = value;

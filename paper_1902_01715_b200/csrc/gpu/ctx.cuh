@@ -76,6 +76,7 @@ struct aspamg_gpu_ctx {
     // C2 0.995 -> 0.966 ms/it, C1 0.120 -> 0.107 ms/it (profiles/tune_r01_tail_long.log)
     long long opt_tail_dense = 1500;
     long long opt_csr_long = 4;  // long-row split threshold in rounds (rows > long*T*4 entries; 0 = off)
+    long long opt_csr_vec = 0;  // 16-bit long-row operands (T >= 16) with the quad-vectorized kernel
     long long opt_csr_pf = 1;  // CSR (T <= 16): prefetch the next row's pointers (measured 1.4% faster per PCG iteration on C2)
     long long opt_rseg = 0, opt_rseg_u = 0, opt_rseg_max_mean = 64, opt_rseg_min_rows = 65536;
     long long opt_idx16 = 1;  // 16-bit column offsets where every row spans < 2^16 columns

@@ -329,6 +329,103 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
 }
 
+// ------------------------------------------------- vectorized 16-bit CSR SpMV
+// Long-row operands with 16-bit column offsets (10 matrix bytes per entry):
+// each thread takes aligned quads of 4 consecutive entries — two 16-B value
+// loads and one 8-B index load per quad instead of four 8-B + four 2-B loads —
+// QU quads per round; the unaligned head / tail entries of a row are handled
+// one per thread. Per-thread fma chains in quad order, then the same fixed
+// shuffle (+ smem for T > 32) tree as k_csr: deterministic, within the CSR
+// tolerance of the reference order.
+template <class T>
+__device__ __forceinline__ T ld_vec(const T* p, int pol) {
+    return pol == 1 ? __ldcs(p) : __ldg(p);
+}
+template <int T, int STREAM, int QU = 2>
+__global__ void __launch_bounds__(kBlock) k_csrv(DCsr M, int epi, const double* __restrict__ x, double* y,
+                                                  const double* aux, double omega, const double* dotw, Red red,
+                                                  const int* done) {
+    pdl_enter();
+    if (is_done(done)) return;
+    constexpr int RPC = kBlock / T;
+    __shared__ double wsum[kBlock / 32];
+    const int t = threadIdx.x % T;
+    const int lr = threadIdx.x / T;
+    const int lane = threadIdx.x & 31;
+    double dacc = 0.0;
+    for (int rbase = blockIdx.x * RPC; rbase < M.n_rows; rbase += gridDim.x * RPC) {
+        const int row = rbase + lr;
+        double s = 0.0;
+        if (row < M.n_rows) {
+            const int b = __ldg(M.rp + row), e = __ldg(M.rp + row + 1);
+            const double* xr = x + __ldg(M.cb + row);
+            const int b4 = min((b + 3) & ~3, e), e4 = max(e & ~3, b4);
+            // head (< 4 entries) and tail (< 4 entries): one entry per thread
+            if (t < b4 - b) {
+                const int k = b + t;
+                s = fma(ld_mat<STREAM>(M.v + k), __ldg(xr + ld_mat<STREAM>(M.ci16 + k)), s);
+            }
+            for (int q0 = b4 + 4 * t; q0 < e4; q0 += 4 * T * QU) {
+                double2 va[QU], vb[QU];
+                ushort4 c[QU];
+#pragma unroll
+                for (int u = 0; u < QU; ++u) {
+                    const int k = q0 + 4 * T * u;
+                    va[u] = make_double2(0.0, 0.0);
+                    vb[u] = va[u];
+                    c[u] = make_ushort4(0, 0, 0, 0);
+                    if (k < e4) {
+                        va[u] = ld_vec(reinterpret_cast<const double2*>(M.v + k), STREAM);
+                        vb[u] = ld_vec(reinterpret_cast<const double2*>(M.v + k + 2), STREAM);
+                        c[u] = ld_vec(reinterpret_cast<const ushort4*>(M.ci16 + k), STREAM);
+                    }
+                }
+                double xv[QU][4];
+#pragma unroll
+                for (int u = 0; u < QU; ++u) {
+                    const bool p = q0 + 4 * T * u < e4;
+                    xv[u][0] = p ? __ldg(xr + c[u].x) : 0.0;
+                    xv[u][1] = p ? __ldg(xr + c[u].y) : 0.0;
+                    xv[u][2] = p ? __ldg(xr + c[u].z) : 0.0;
+                    xv[u][3] = p ? __ldg(xr + c[u].w) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < QU; ++u) {
+                    s = fma(va[u].x, xv[u][0], s);
+                    s = fma(va[u].y, xv[u][1], s);
+                    s = fma(vb[u].x, xv[u][2], s);
+                    s = fma(vb[u].y, xv[u][3], s);
+                }
+            }
+            if (t < e - e4) {
+                const int k = e4 + t;
+                s = fma(ld_mat<STREAM>(M.v + k), __ldg(xr + ld_mat<STREAM>(M.ci16 + k)), s);
+            }
+        }
+        if constexpr (T <= 32) {
+#pragma unroll
+            for (int o = T / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, T);
+        } else {
+            s = warp_sum(s);
+            if (lane == 0) wsum[threadIdx.x >> 5] = s;
+            __syncthreads();
+            if (t == 0) {
+                double a = 0.0;
+#pragma unroll
+                for (int w = 0; w < T / 32; ++w) a += wsum[(threadIdx.x >> 5) + w];
+                s = a;
+            }
+            __syncthreads();
+        }
+        if (t == 0 && row < M.n_rows) {
+            const double out = epilogue(epi, s, aux, row, omega);
+            y[row] = out;
+            if (dotw) dacc = fma(out, dotw[row], dacc);
+        }
+    }
+    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
+}
+
 // ---------------------------------------------------- row-segment CSR SpMV
 // A warp owns 32 consecutive rows (lane l <-> row r0 + l). Their entries form
 // one contiguous CSR segment [rp[r0], rp[r0+32]); the warp streams it in tiles
@@ -1159,6 +1256,9 @@ int occ_grid(K kern, long long work_units_per_cta_needed, size_t smem = 0) {
 using SpmvKern = void (*)(DCsr, int, const double*, double*, const double*, double, const double*, Red, const int*);
 template <int GG, int P, bool I16>
 SpmvKern csr_kernel_i(const DCsr& A) {
+    if constexpr (I16 && GG >= 16) {
+        if (A.vec) return k_csrv<GG, P>;
+    }
     const bool u8 = A.u8 == 2 || (A.u8 == 1 && GG >= 32);
     if constexpr (GG <= 16) {
         if (A.pf) return u8 ? k_csr<GG, P, I16, 8, true> : k_csr<GG, P, I16, 4, true>;

@@ -36,6 +36,7 @@ struct DCsr {
     int rseg = 0;
     int u8 = 0;  // k_csr with 8 loads per thread per round (1: T >= 32, 2: every T)
     int pf = 0;  // k_csr row-pointer prefetch (T <= 16)
+    int vec = 0;  // k_csrv: quad-vectorized loads (16-bit offsets, T >= 16)
     // Long-row split: rows longer than lthr (listed in lrows) are computed by the
     // first nlctas CTAs of the launch, one warp per row; the regular T-thread
     // groups skip them, so a long-tailed operand (G' rows up to ~7x the mean) no

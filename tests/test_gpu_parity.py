@@ -361,3 +361,21 @@ def test_dense_coarse_tail_matches_oracle(pkg, oracle, rows):
     assert rel_err(g.apply(y), o.vcycle(y)) < RTOL_VCYCLE
     assert np.array_equal(g.apply(y), g.apply(y))
     _pcg_parity(p, h, g, o)
+
+
+@pytest.mark.parametrize("opts", [{"csr_vec": 1}, {"csr_vec": 1, "csr_long": 0}])
+def test_csr_vectorized_16bit_matches_oracle(pkg, oracle, opts):
+    """Quad-vectorized 16-bit CSR kernel (k_csrv) for long-row operands: every
+    operand within the CSR per-row bound, PCG within the north_star tolerances."""
+    p, h = problem_and_hierarchy(2, 2)
+    g = _gpu(pkg, h, **opts)
+    o = _oracle(oracle, h)
+    rng = np.random.default_rng(19)
+    for l in range(h.n_levels - 1):
+        for wi, which in enumerate(["A", "G", "Gt", "P", "Pt"]):
+            m = getattr(h.level(l, copy=False), which)
+            x = rng.standard_normal(m.n_cols)
+            yg, yo = g.spmv(l, wi, x), o.spmv(l, which, x)
+            absrow = np.abs(m.to_scipy()) @ np.abs(x)
+            assert np.all(np.abs(yg - yo) <= 1e-14 * absrow + 1e-300), (opts, which, l)
+    _pcg_parity(p, h, g, o)
