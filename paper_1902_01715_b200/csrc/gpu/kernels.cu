@@ -794,6 +794,11 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const d
             for (int u = 0; u < U; ++u)
                 if (u < rem) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
         }
+        if (cu.w <= 0 && chn < M.nchunks) {  // all-empty group: the loop above never prefetched the next chunk
+            const CT* np = colb + nx.base;
+#pragma unroll
+            for (int u = 0; u < U; ++u) cn[u] = (u < nx.len) ? (int)ld_mat<STREAM>(np + SS * u) : 0;
+        }
         if (cu.act) {
             double out;
             switch (epi) {
