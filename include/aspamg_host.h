@@ -114,7 +114,9 @@ int aspamg_galerkin(const aspamg_csr_view* P, const aspamg_csr_view* A, aspamg_c
  * adaptive FSAI set-up through fn (e.g. aspamg_gpu_smoother_setup); the host forms the
  * Kaporin estimate from the returned psi. fn may return -1 to decline a level (the
  * host then computes it) or -2 to hand back the refinement loop after its last finished
- * pass (the host continues it). NULL restores the CPU path. Process-wide. */
+ * pass (the host continues it; G's rows then arrive in insertion order — the pattern in
+ * the order its entries were added, then the diagonal — which is the factor order the
+ * next pass restarts from). NULL restores the CPU path. Process-wide. */
 typedef int (*aspamg_smoother_fn)(void* user, const aspamg_csr_view* A, const aspamg_smoother_params* prm,
                                   aspamg_csr_alloc_fn alloc, void* sink, double* psi, double* omega,
                                   double* lambda_hat, int64_t* passes, int* exit_reason);
@@ -123,6 +125,13 @@ int aspamg_set_smoother_backend(aspamg_smoother_fn fn, void* user);
  * buffer set; G_out views stay valid until aspamg_csr_free. */
 int aspamg_afsai_build(const aspamg_csr_view* A, int64_t k, int64_t rho, double eps, aspamg_csr_owned** G,
                        aspamg_csr_view* G_view);
+/* smoother_setup (Alg. 3) of one operator on the host (through the
+ * registered smoother backend, if any): G (free with aspamg_csr_free), omega,
+ * lambda_hat, refinement passes and exit reason (0 omega reached, 1 density bound,
+ * 2 pattern stagnation). */
+int aspamg_smoother_setup(const aspamg_csr_view* A, const aspamg_setup_config* cfg, aspamg_csr_owned** G,
+                          aspamg_csr_view* G_view, double* omega, double* lambda_hat, int64_t* passes,
+                          int* exit_reason);
 /* Lanczos estimate of lambda_max(G A G') x 1.05. */
 int aspamg_estimate_lambda_max(const aspamg_csr_view* G, const aspamg_csr_view* A, int64_t steps, uint64_t seed,
                                double* lambda_hat);

@@ -107,6 +107,8 @@ def host() -> C.CDLL:
         lib.aspamg_srqcg.argtypes = [C.POINTER(CsrView), C.POINTER(CsrView), P_dbl, i64, i64, i64, dbl, C.c_uint64,
                                      P_dbl, P_dbl, P_i64]
         lib.aspamg_afsai_build.argtypes = [C.POINTER(CsrView), i64, i64, dbl, C.POINTER(C.c_void_p), C.POINTER(CsrView)]
+        lib.aspamg_smoother_setup.argtypes = [C.POINTER(CsrView), C.POINTER(SetupConfig), C.POINTER(C.c_void_p),
+                                              C.POINTER(CsrView), P_dbl, P_dbl, P_i64, C.POINTER(C.c_int)]
         lib.aspamg_estimate_lambda_max.argtypes = [C.POINTER(CsrView), C.POINTER(CsrView), i64, C.c_uint64, P_dbl]
         lib.aspamg_csr_free.argtypes = [C.c_void_p]
         lib.aspamg_csr_free.restype = None

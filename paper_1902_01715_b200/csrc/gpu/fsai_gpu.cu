@@ -49,6 +49,8 @@ struct AfsaiArgs {
     int* cnt = nullptr;          // per row: m + 1 entries; -1 not SPD; -2 table overflow
     long long* ocol = nullptr;   // n x (mcap + 1) scratch, row sorted by column
     double* oval = nullptr;
+    long long* ocol_ins = nullptr;  // the same rows in insertion order (pattern, then i)
+    double* oval_ins = nullptr;
     double* psi = nullptr;
     unsigned long long* bad = nullptr;  // smallest failing row
 };
@@ -374,6 +376,8 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
         if (e < m) rank += i < col;
         P.ocol[base + rank] = col;
         P.oval[base + rank] = val;
+        P.ocol_ins[base + e] = col;
+        P.oval_ins[base + e] = val;
     }
     if (lane == 0) {
         P.cnt[i] = m + 1;
@@ -475,6 +479,7 @@ __global__ void k_lanczos_upd(long long n, double* w, const double* __restrict__
 
 struct DevG {  // a device CSR the setup owns, plus its host row offsets
     DevCsr d;
+    DevCsr ins;  // the same rows in insertion order (the next pass's start pattern); shares d.rp
     std::vector<long long> rp;
 };
 
@@ -483,6 +488,13 @@ void free_csr(aspamg_gpu_ctx* c, DevCsr& d) {
     dfree(c, d.ci);
     dfree(c, d.v);
     d = DevCsr{};
+}
+
+void free_g(aspamg_gpu_ctx* c, DevG& g) {
+    dfree(c, g.ins.ci);
+    dfree(c, g.ins.v);
+    g.ins = DevCsr{};
+    free_csr(c, g.d);
 }
 
 int sm_count() {
@@ -507,6 +519,8 @@ DevG afsai_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const 
     int* cnt = dalloc<int>(c, (size_t)std::max<long long>(n, 1));
     long long* ocol = dalloc<long long>(c, (size_t)std::max<long long>(n, 1) * rowcap);
     double* oval = dalloc<double>(c, (size_t)std::max<long long>(n, 1) * rowcap);
+    long long* ocol_ins = dalloc<long long>(c, (size_t)std::max<long long>(n, 1) * rowcap);
+    double* oval_ins = dalloc<double>(c, (size_t)std::max<long long>(n, 1) * rowcap);
     unsigned long long* bad = dalloc<unsigned long long>(c, 1);
     const unsigned long long none = ~0ull;
     CK(cudaMemcpyAsync(bad, &none, 8, cudaMemcpyHostToDevice, s));
@@ -522,7 +536,7 @@ DevG afsai_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const 
         AfsaiArgs P;
         P.A = A;
         P.gs_rp = Gs ? Gs->d.rp : nullptr;
-        P.gs_ci = Gs ? Gs->d.ci : nullptr;
+        P.gs_ci = Gs ? Gs->ins.ci : nullptr;  // factor order = insertion order (fsai.cpp run_row)
         P.k = k;
         P.rho = rho;
         P.eps = eps;
@@ -531,6 +545,8 @@ DevG afsai_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const 
         P.cnt = cnt;
         P.ocol = ocol;
         P.oval = oval;
+        P.ocol_ins = ocol_ins;
+        P.oval_ins = oval_ins;
         P.psi = psi;
         P.bad = bad;
         long long* drows = nullptr;
@@ -583,15 +599,21 @@ DevG afsai_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const 
     G.d.ci = dalloc<long long>(c, (size_t)std::max<long long>(nnz, 1));
     G.d.v = dalloc<double>(c, (size_t)std::max<long long>(nnz, 1));
     CK(cudaMemcpyAsync(G.d.rp, G.rp.data(), G.rp.size() * 8, cudaMemcpyHostToDevice, s));
+    G.ins.ci = dalloc<long long>(c, (size_t)std::max<long long>(nnz, 1));
+    G.ins.v = dalloc<double>(c, (size_t)std::max<long long>(nnz, 1));
     k_compact<<<sms * 8, 256, 0, s>>>(n, G.d.rp, rowcap, ocol, oval, G.d.ci, G.d.v);
+    k_compact<<<sms * 8, 256, 0, s>>>(n, G.d.rp, rowcap, ocol_ins, oval_ins, G.ins.ci, G.ins.v);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     for (void* q : scratch) dfree(c, q);
     dfree(c, cnt);
     dfree(c, ocol);
     dfree(c, oval);
+    dfree(c, ocol_ins);
+    dfree(c, oval_ins);
     dfree(c, bad);
     G.d.view = {n, n, nnz, G.d.rp, G.d.ci, G.d.v};
+    G.ins.view = {n, n, nnz, G.d.rp, G.ins.ci, G.ins.v};
     return G;
 }
 
@@ -754,11 +776,11 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
             if (!(nnz_r < prm->rho_bar)) { ex = 1; break; }  // density_bound
             DevG G2 = afsai_device(c, dA.view, a_maxrow, &G, (int)prm->ki, (int)prm->rhoi, prm->epsi, psi2);
             if (G2.d.view.nnz == G.d.view.nnz) {  // pattern_stagnation
-                free_csr(c, G2.d);
+                free_g(c, G2);
                 ex = 2;
                 break;
             }
-            free_csr(c, G.d);
+            free_g(c, G);
             free_csr(c, Gt);
             G = std::move(G2);
             std::swap(psi, psi2);
@@ -773,10 +795,12 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
         const long long nnz = G.d.view.nnz;
         if (alloc(sink, n, n, nnz, &rp, &ci, &vals) != 0 || !rp || (nnz && (!ci || !vals)))
             throw Fail{5, "smoother_setup: output allocation failed"};
+        // finished: sorted rows; handed back: insertion order (the host restarts from it)
+        const DevCsr& out = handed ? G.ins : G.d;
         CK(cudaMemcpyAsync(rp, G.d.rp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
         if (nnz) {
-            CK(cudaMemcpyAsync(ci, G.d.ci, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaMemcpyAsync(vals, G.d.v, sizeof(double) * nnz, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(ci, out.ci, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(vals, out.v, sizeof(double) * nnz, cudaMemcpyDeviceToHost, c->stream));
         }
         CK(cudaMemcpyAsync(psi_out, psi, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));

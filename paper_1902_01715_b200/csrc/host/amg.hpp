@@ -39,7 +39,9 @@ struct FsaiSmoother {  // fsai.hpp:44-53
     SmootherExit exit_reason = SmootherExit::omega_reached;
 };
 
-// SPEC.md:172-180 (fsai.hpp:61-66). G_start == nullptr means identity start.
+// SPEC.md:172-180 (fsai.hpp:61-66). G_start == nullptr means identity start; otherwise
+// each row's start pattern (columns < i) is taken in G_start's stored order, which is
+// the order of the row's incremental factor (smoother_setup passes insertion order).
 Csr afsai_build(const Csr& A, const Csr* G_start, index_t k, index_t rho, double eps,
                 std::vector<double>* psi_out = nullptr);
 // SPEC.md:181-189 (fsai.hpp:68-71): Lanczos on G A G', x1.05.
@@ -50,9 +52,11 @@ FsaiSmoother smoother_setup(const Csr& A, const SmootherConfig& cfg);  // SPEC.m
 // returns G, omega, lambda_hat, passes, exit reason, and psi (for the Kaporin estimate).
 bool smoother_backend_set();
 // 0: the backend declined (status -1), the host computes the level; 1: complete;
-// 2: handed back after a finished pass (status -2), the host continues the refinement loop.
+// 2: handed back after a finished pass (status -2), the host continues the refinement loop;
+// the backend then delivers G's rows in insertion order (pattern, then i): G is sorted
+// here and *ord receives the insertion-ordered twin (the next pass's start pattern).
 int smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi,
-                      FsaiSmoother& out);
+                      FsaiSmoother& out, Csr* ord);
 // x' = x + omega G'(G(b - A x)) (host reference; Gt explicit)
 std::vector<double> apply_smoothing_step(const Csr& G, const Csr& Gt, double omega, const Csr& A,
                                          const std::vector<double>& b, const std::vector<double>& x);

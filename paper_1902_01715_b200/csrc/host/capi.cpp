@@ -4,6 +4,7 @@
 #include "amg.hpp"
 #include "fem.hpp"
 
+#include <algorithm>
 #include <new>
 #include <string>
 
@@ -229,6 +230,32 @@ int aspamg_afsai_build(const aspamg_csr_view* A, int64_t k, int64_t rho, double 
     });
 }
 
+int aspamg_smoother_setup(const aspamg_csr_view* A, const aspamg_setup_config* c, aspamg_csr_owned** G,
+                          aspamg_csr_view* G_view, double* omega, double* lambda_hat, int64_t* passes,
+                          int* exit_reason) {
+    return guard([&] {
+        if (!A || !c || !G || !G_view || !omega || !lambda_hat || !passes || !exit_reason)
+            throw ConfigError("aspamg_smoother_setup: null argument");
+        SmootherConfig sc;
+        sc.k0 = c->k0; sc.rho0 = c->rho0; sc.eps0 = c->eps0;
+        sc.ki = c->ki; sc.rhoi = c->rhoi; sc.epsi = c->epsi;
+        sc.omega_bar = c->omega_bar; sc.rho_bar = c->rho_bar;
+        sc.lanczos_steps = c->lanczos_steps; sc.seed = c->seed;
+        Csr a = from_view(*A);
+        auto* o = new aspamg_csr_owned;
+        try {
+            FsaiSmoother sm = smoother_setup(a, sc);
+            o->m = std::move(sm.G);
+            *omega = sm.omega;
+            *lambda_hat = sm.lambda_hat;
+            *passes = sm.refinement_passes;
+            *exit_reason = static_cast<int>(sm.exit_reason);
+        } catch (...) { delete o; throw; }
+        *G = o;
+        *G_view = view(o->m);
+    });
+}
+
 int aspamg_estimate_lambda_max(const aspamg_csr_view* G, const aspamg_csr_view* A, int64_t steps, uint64_t seed,
                                double* lambda_hat) {
     return guard([&] {
@@ -356,7 +383,7 @@ namespace aspamg {
 bool smoother_backend_set() { return g_smoother_fn != nullptr; }
 
 int smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, std::vector<double>& psi,
-                      FsaiSmoother& out) {
+                      FsaiSmoother& out, Csr* ord) {
     const aspamg_csr_view a = view(A);
     aspamg_smoother_params prm{cfg.k0, cfg.rho0, cfg.eps0, cfg.ki, cfg.rhoi, cfg.epsi,
                                cfg.omega_bar, rho_bar, cfg.lanczos_steps, cfg.seed};
@@ -377,6 +404,30 @@ int smoother_external(const Csr& A, const SmootherConfig& cfg, double rho_bar, s
     }
     s.refinement_passes = passes;
     s.exit_reason = static_cast<SmootherExit>(exit_reason);
+    if (st == -2) {  // handed back: rows arrive in insertion order (the pattern, then i)
+        Csr& G = s.G;
+        if (ord) {
+            ord->n_rows = ord->n_cols = G.n_rows;
+            ord->rowptr = G.rowptr;
+            ord->col = G.col;
+            ord->val.clear();
+        }
+#pragma omp parallel num_threads(num_threads())
+        {
+            std::vector<std::pair<index_t, double>> e;
+#pragma omp for schedule(dynamic, 1024)
+            for (index_t i = 0; i < G.n_rows; ++i) {
+                e.clear();
+                for (index_t q = G.row_begin(i); q < G.row_end(i); ++q)
+                    e.emplace_back(G.col[static_cast<size_t>(q)], G.val[static_cast<size_t>(q)]);
+                std::sort(e.begin(), e.end());
+                for (size_t q = 0; q < e.size(); ++q) {
+                    G.col[static_cast<size_t>(G.row_begin(i)) + q] = e[q].first;
+                    G.val[static_cast<size_t>(G.row_begin(i)) + q] = e[q].second;
+                }
+            }
+        }
+    }
     out = std::move(s);
     return st == -2 ? 2 : 1;
 }

@@ -60,26 +60,68 @@ void spmv(const Csr& A, const double* x, double* y) {
     }
 }
 
-// sparse_matrix.cpp:168-189 (counting sort; rows of T in ascending source row)
+// sparse_matrix.cpp:168-189 (counting sort; rows of T in ascending source row).
+// Parallel over contiguous source-row chunks: chunk t's entries of column c go
+// after those of chunks < t, so every row of T is still in ascending source row
+// (the same T as the sequential counting sort).
 Csr transpose(const Csr& A) {
     Csr T;
+    transpose_into(A, T);
+    return T;
+}
+
+void transpose_into(const Csr& A, Csr& T) {
     T.n_rows = A.n_cols;
     T.n_cols = A.n_rows;
     T.symmetric = A.symmetric;
-    T.rowptr.assign(static_cast<size_t>(A.n_cols) + 1, 0);
+    const size_t nc = static_cast<size_t>(A.n_cols);
+    T.rowptr.assign(nc + 1, 0);
     T.col.resize(A.col.size());
     T.val.resize(A.val.size());
-    for (index_t c : A.col) ++T.rowptr[static_cast<size_t>(c) + 1];
-    std::partial_sum(T.rowptr.begin(), T.rowptr.end(), T.rowptr.begin());
-    std::vector<index_t> cur(T.rowptr.begin(), T.rowptr.end() - 1);
-    for (index_t i = 0; i < A.n_rows; ++i)
-        for (index_t k = A.row_begin(i); k < A.row_end(i); ++k) {
-            const index_t j = A.col[static_cast<size_t>(k)];
-            const index_t p = cur[static_cast<size_t>(j)]++;
-            T.col[static_cast<size_t>(p)] = i;
-            T.val[static_cast<size_t>(p)] = A.val[static_cast<size_t>(k)];
+    const size_t nnz = A.col.size();
+    int nt = (nnz < (1u << 20) || nc == 0) ? 1 : std::min(num_threads(), 16);
+    // chunk boundaries by nnz
+    std::vector<index_t> rb(static_cast<size_t>(nt) + 1, A.n_rows);
+    rb[0] = 0;
+    for (int t = 1; t < nt; ++t) {
+        const index_t target = static_cast<index_t>(nnz * static_cast<size_t>(t) / static_cast<size_t>(nt));
+        rb[static_cast<size_t>(t)] = std::lower_bound(A.rowptr.begin(), A.rowptr.end(), target) - A.rowptr.begin();
+        rb[static_cast<size_t>(t)] = std::min(std::max(rb[static_cast<size_t>(t)], rb[static_cast<size_t>(t) - 1]), A.n_rows);
+    }
+    std::vector<std::vector<index_t>> cnt(static_cast<size_t>(nt));
+#pragma omp parallel num_threads(nt)
+    {
+        const int tid = omp_get_thread_num(), nthr = omp_get_num_threads();
+        for (int t = tid; t < nt; t += nthr) {  // chunk t (the team may be smaller than nt)
+            std::vector<index_t>& c = cnt[static_cast<size_t>(t)];
+            c.assign(nc, 0);
+            for (index_t k = A.row_begin(rb[static_cast<size_t>(t)]); k < A.row_begin(rb[static_cast<size_t>(t) + 1]); ++k)
+                ++c[static_cast<size_t>(A.col[static_cast<size_t>(k)])];
         }
-    return T;
+#pragma omp barrier
+#pragma omp for schedule(static)
+        for (size_t j = 0; j < nc; ++j) {  // per column: chunk offsets (exclusive), total
+            index_t s = 0;
+            for (int u = 0; u < nt; ++u) {
+                const index_t v = cnt[static_cast<size_t>(u)][j];
+                cnt[static_cast<size_t>(u)][j] = s;
+                s += v;
+            }
+            T.rowptr[j + 1] = s;
+        }
+#pragma omp single
+        std::partial_sum(T.rowptr.begin(), T.rowptr.end(), T.rowptr.begin());
+        for (int t = tid; t < nt; t += nthr) {
+            std::vector<index_t>& c = cnt[static_cast<size_t>(t)];
+            for (index_t i = rb[static_cast<size_t>(t)]; i < rb[static_cast<size_t>(t) + 1]; ++i)
+                for (index_t k = A.row_begin(i); k < A.row_end(i); ++k) {
+                    const size_t j = static_cast<size_t>(A.col[static_cast<size_t>(k)]);
+                    const index_t p = T.rowptr[j] + c[j]++;
+                    T.col[static_cast<size_t>(p)] = i;
+                    T.val[static_cast<size_t>(p)] = A.val[static_cast<size_t>(k)];
+                }
+        }
+    }
 }
 
 // sparse_matrix.cpp:132-166. Row-parallel: each thread owns a dense

@@ -56,6 +56,7 @@ struct Csr {
 void spmv(const Csr& A, const double* x, double* y);
 // Counting-sort transpose (sparse_matrix.cpp:168-189 semantics: deterministic).
 Csr transpose(const Csr& A);
+void transpose_into(const Csr& A, Csr& T);  // same, reusing T's buffers
 // C = A B, per-row accumulator; first-touch order; sorted output
 // (sparse_matrix.cpp:132-166 semantics, row-parallel).
 Csr sparse_multiply(const Csr& A, const Csr& B);

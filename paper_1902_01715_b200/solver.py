@@ -536,6 +536,23 @@ def gpu_setup_policy(key: str, value: float) -> None:
         _raise(st, N.gpu().aspamg_gpu_last_error(None).decode())
 
 
+def host_smoother_setup(A: SparseMatrix, cfg: Optional[N.SetupConfig] = None) -> dict:
+    """fsai.cpp smoother_setup (Alg. 3) of one operator on the host."""
+    cfg = cfg or default_config()
+    h = C.c_void_p()
+    gv = N.CsrView()
+    om, lam = C.c_double(), C.c_double()
+    passes, ex = C.c_int64(), C.c_int()
+    av = A.view()
+    _chk_host(N.host().aspamg_smoother_setup(C.byref(av), C.byref(cfg), C.byref(h), C.byref(gv), C.byref(om),
+                                             C.byref(lam), C.byref(passes), C.byref(ex)))
+    try:
+        G = SparseMatrix.from_view(gv, copy=True)
+    finally:
+        N.host().aspamg_csr_free(h)
+    return {"G": G, "omega": om.value, "lambda_hat": lam.value, "passes": passes.value, "exit": ex.value}
+
+
 def host_galerkin(P: SparseMatrix, A: SparseMatrix) -> SparseMatrix:
     """The host restatement of galerkin_triple (sparse_matrix.cpp:191-199)."""
     pv, av = P.view(), A.view()

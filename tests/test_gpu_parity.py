@@ -379,3 +379,55 @@ def test_csr_vectorized_16bit_matches_oracle(pkg, oracle, opts):
             absrow = np.abs(m.to_scipy()) @ np.abs(x)
             assert np.all(np.abs(yg - yo) <= 1e-14 * absrow + 1e-300), (opts, which, l)
     _pcg_parity(p, h, g, o)
+
+
+def test_sell_all_empty_row_groups(pkg):
+    """A SELL-32 operand whose 32-row groups are alternately all-empty and
+    populated, with more chunks than resident warps (each warp walks several
+    chunks): the next chunk's column prefetch must not be skipped by an empty
+    group. Products checked exactly against scipy (one entry per
+    row or ascending sequential sums of exactly representable values)."""
+    import ctypes as C
+    import scipy.sparse as sp
+    from paper_1902_01715_b200 import _native as N
+    lib = N.gpu()
+    rng = np.random.default_rng(23)
+    n, nc = 32 * 12000, 64
+    rows, cols, vals = [], [], []
+    for g in range(n // 32):
+        if g % 3 == 1:
+            continue  # all 32 rows of this group empty
+        for r in range(32 * g, 32 * g + 32):
+            k = 1 + (r % 3)
+            cs = np.sort(rng.choice(nc, size=k, replace=False))
+            rows += [r] * k
+            cols += list(cs)
+            vals += list(rng.integers(1, 8, size=k).astype(float))
+    Pm = sp.csr_matrix((vals, (rows, cols)), shape=(n, nc))
+    Pm.sort_indices()
+    I = sp.identity(n, format="csr")
+    Ic = sp.identity(nc, format="csr")
+    mats0 = [pkg.SparseMatrix.from_scipy(m) for m in (I, I, I, Pm, Pm.T.tocsr())]
+    empty = pkg.SparseMatrix(0, 0, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    mats1 = [pkg.SparseMatrix.from_scipy(Ic)] + [empty] * 4
+    ctx = C.c_void_p()
+    assert lib.aspamg_gpu_ctx_create(0, C.byref(ctx)) == 0
+    try:
+        for k, v in {"sell_min_rows": 0, "sell_min_mean": 0, "sell_chh": 32, "bsr": 0, "tail_dense": 0}.items():
+            assert lib.aspamg_gpu_set_option(ctx, k.encode(), v) == 0
+        for l, ms in enumerate((mats0, mats1)):
+            views = [m.view() for m in ms]
+            assert lib.aspamg_gpu_upload_level(ctx, l, *[C.byref(v) for v in views], 1.0) == 0
+        L = np.ascontiguousarray(np.eye(nc).ravel(order="F"))
+        assert lib.aspamg_gpu_upload_coarse(ctx, nc, L.ctypes.data_as(C.POINTER(C.c_double))) == 0
+        assert lib.aspamg_gpu_finalize(ctx) == 0
+        info = N.GpuLevelInfo()
+        assert lib.aspamg_gpu_level_info(ctx, 0, C.byref(info)) == 0
+        assert info.fmt[3] == 2, "P must be uploaded as SELL for this test"
+        x = rng.integers(-4, 5, size=nc).astype(float)
+        y = np.empty(n)
+        P_d = C.POINTER(C.c_double)
+        assert lib.aspamg_gpu_spmv(ctx, 0, 3, x.ctypes.data_as(P_d), y.ctypes.data_as(P_d)) == 0
+        assert np.array_equal(y, Pm @ x)
+    finally:
+        lib.aspamg_gpu_ctx_destroy(ctx)
