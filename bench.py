@@ -1,21 +1,24 @@
 #!/usr/bin/env python3
 """Benchmark of the solve phase: PCG + aSP-AMG V(1,1)-cycle on one B200.
 
-A "step" is one full PCG solve (x0 = 0 -> ||r|| <= 1e-8 ||b||) of the
-BASELINE.json configs[1] workload (C2: 64^3 hex cube, 8^3-element blocks with
-log-uniform E in [1, 1e6], clamped z=0, top load) on the hierarchy produced
-once by the CPU setup and uploaded once. ``value`` is seconds per PCG
-iteration over the timed solves (inputs resident in HBM); ``ms_per_step`` is
-the time-to-1e-8. ``e2e`` is the same metric through the C-ABI call with host
-buffers (H2D of b, D2H of x and the residual history inside the timed region).
+A "step" is one full PCG solve (x0 = 0 -> ||r|| <= 1e-8 ||b||) of the largest
+single-GPU BASELINE.json config (default C5: 128^3 hex cube, 200 stiff spheres,
+6.39M dofs, 0.51B nnz; --config selects another) on the hierarchy produced once
+by the setup and uploaded once. ``value`` is seconds per PCG iteration over the
+timed solves (inputs resident in HBM); ``ms_per_step`` and ``time_to_1e8_s``
+are the time-to-1e-8 of one solve. ``e2e`` is the same metric through the
+C-ABI call with host buffers (H2D of b, D2H of x and the residual history
+inside the timed region).
 
 ``--impl reference`` times the reference's CPU path on the host cores: the
 restated pcg / vcycle_apply (oracle/oracle.c) driving the reference's own
 compiled spmv (oracle/_ref, sparse_matrix.cpp:96-107), each step a bounded
-sample of PCG iterations of the same workload.
+sample of PCG iterations of the same workload. Both arms print the same
+``metric`` string and unit (s/iteration), so the ratio is per PCG iteration.
 
 Multi-GPU (torchrun, N > 1): replicas only — every rank solves
-the same problem independently; times are the max over ranks.
+the same problem independently; ``value`` is the slowest rank's s/iteration,
+``job_iterations_per_s`` the aggregate throughput of all replicas.
 """
 from __future__ import annotations
 
@@ -34,6 +37,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+
+METRIC = "PCG+AMG solve: s/iteration"
 
 CONFIG_DESC = {
     1: "C1: 20^3 hex unit cube, E=1 nu=0.3, clamp z=0, top f_z=-1",
@@ -103,8 +108,10 @@ def file_hash(path):
 
 def get_hierarchy(P, cfg, scale, rank, dist, threads, setup_device=None):
     """Setup once (rank 0), cached on disk for the other ranks / reruns. With
-    setup_device the SRQCG and Galerkin phases run on that GPU (bit-identical
-    hierarchy, tests/test_gpu_setup.py)."""
+    setup_device the SRQCG, aFSAI and Galerkin phases run on that GPU (the
+    identical hierarchy, tests/test_gpu_setup.py). Returns the setup's origin
+    ("cpu", "cpu + gpu (...)", or the origin recorded when the cached file was
+    written) with it."""
     from paper_1902_01715_b200 import _native as N
     t0 = time.perf_counter()
     prob = P.Problem.config(cfg, scale)
@@ -113,20 +120,28 @@ def get_hierarchy(P, cfg, scale, rank, dist, threads, setup_device=None):
     os.makedirs(cache_dir, exist_ok=True)
     key = f"hier_c{cfg}_s{scale}_{file_hash(os.path.join(N.LIB_DIR, 'libaspamg_host.so'))}.bin"
     path = os.path.join(cache_dir, key)
+    origin = "cpu" if setup_device is None else "cpu + gpu (srqcg, afsai, galerkin)"
     t_setup = None
     if rank == 0 and not os.path.exists(path):
         t0 = time.perf_counter()
         h = P.Hierarchy.setup(prob.K, prob.coords, threads=threads, setup_device=setup_device)
         t_setup = time.perf_counter() - t0
         if os.environ.get("ASPAMG_NO_CACHE"):  # single-process runs of huge configs: skip the dump
-            return prob, h, t_gen, t_setup
+            return prob, h, t_gen, t_setup, origin
         h.save(path + ".tmp")
+        with open(path + ".json", "w") as f:
+            json.dump({"origin": origin, "setup_s": t_setup}, f)
         os.replace(path + ".tmp", path)
     dist.barrier()
     if t_setup is None:
         h = P.Hierarchy.load(path)
         t_setup = h.info().T_p
-    return prob, h, t_gen, t_setup
+        try:
+            with open(path + ".json") as f:
+                origin = "cached: " + json.load(f)["origin"]
+        except Exception:
+            origin = "cached (origin unrecorded)"
+    return prob, h, t_gen, t_setup, origin
 
 
 class ClockSampler:
@@ -205,6 +220,16 @@ def cpu_reference_sample(h, rhs, threads, target_s=12.0, max_iters=60):
     return oh, use_ref, iters
 
 
+def cpu_one_thread(h, rhs, target_s=10.0):
+    """The same CPU path on ONE thread (the reference parallel_for spawns threads per
+    call, parallel.hpp:41-57; coarse levels are spawn-bound): a short sample."""
+    oh, use_ref, iters = cpu_reference_sample(h, rhs, 1, target_s=target_s, max_iters=20)
+    t0 = time.perf_counter()
+    oh.pcg(rhs, rel_tol=0.0, max_it=iters)
+    return {"value": (time.perf_counter() - t0) / iters, "unit": "s/iteration", "cores": 1,
+            "sample": f"{iters} PCG iterations"}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return 0
@@ -215,7 +240,9 @@ def run_reference(args, ws, rank):
             pass
 
     threads = os.cpu_count() or 1
-    prob, h, t_gen, t_setup = get_hierarchy(P, args.config, args.scale, 0, _D(), threads)
+    # the hierarchy is the solve's INPUT (north_star: produced by the CPU setup);
+    # only the solve below is timed
+    prob, h, t_gen, t_setup, origin = get_hierarchy(P, args.config, args.scale, 0, _D(), threads)
     oh, use_ref, iters = cpu_reference_sample(h, prob.rhs, threads, target_s=args.ref_sample_s)
     times, its = [], 0
     for step in range(args.warmup + args.steps):
@@ -228,22 +255,33 @@ def run_reference(args, ws, rank):
     value = sum(times) / its
     kind = "reference" if use_ref else "port"
     sample = (f"{iters} PCG iterations per step (x0=0, same hierarchy as the GPU arm) of "
-              f"{'restated pcg/vcycle_apply (oracle/oracle.c) on the reference spmv compiled from sparse_matrix.cpp' if use_ref else 'the oracle port'}; "
-              f"full solve is ~{args.full_iters or 'n_it'} iterations")
+              f"{'restated pcg/vcycle_apply (oracle/oracle.c) on the reference spmv compiled from sparse_matrix.cpp' if use_ref else 'the oracle port'}")
     line = {
         "impl": "reference",
-        "metric": "PCG+AMG solve: s/iteration (time-to-1e-8 = s/it x n_it)",
+        "metric": METRIC,
         "value": value, "unit": "s/iteration", "higher_is_better": False,
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(times) / len(times), "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": 1e3 * sum(times) / len(times), "ms_per_step_is": f"one step = {iters} PCG iterations",
+        "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIG_DESC[args.config], "n": prob.K.n_rows, "nnz": prob.K.nnz,
-                   "scale": args.scale, "setup_s": t_setup, "l2": "inputs larger than L2 (K alone > 126 MB)" if args.config != 1 else "K fits L2"},
+                   "scale": args.scale, "setup_s": t_setup, "setup_on": origin,
+                   "l2": "inputs larger than L2 (K alone > 126 MB)" if args.config != 1 else "K fits L2"},
         "cpu_baseline": {"value": value, "unit": "s/iteration", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "s/iteration", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def kernel_build_tag():
+    """Hash of the solve kernels' sources: profiles/traffic.json entries (ncu DRAM
+    bytes per launch) are only reported for the build they were captured on."""
+    hh = hashlib.sha1()
+    for f in ("kernels.cu", "kernels.cuh", "context.cu"):
+        with open(os.path.join(ROOT, "paper_1902_01715_b200", "csrc", "gpu", f), "rb") as fh:
+            hh.update(fh.read())
+    return hh.hexdigest()[:12]
 
 
 def run_b200(args, ws, rank, local):
@@ -253,8 +291,8 @@ def run_b200(args, ws, rank, local):
     threads = max(1, (os.cpu_count() or 1) // max(1, ws))
     # setup (outside the timed region): CPU, with the SRQCG + Galerkin phases on this
     # rank's GPU — the identical hierarchy the all-CPU setup builds (tests/test_gpu_setup.py)
-    prob, h, t_gen, t_setup = get_hierarchy(P, args.config, args.scale, rank, dist, os.cpu_count() or 1,
-                                            None if args.cpu_setup else local)
+    prob, h, t_gen, t_setup, origin = get_hierarchy(P, args.config, args.scale, rank, dist, os.cpu_count() or 1,
+                                                    None if args.cpu_setup else local)
     info = h.info()
     t0 = time.perf_counter()
     g = P.GpuVcycle(h, device=local)
@@ -304,9 +342,12 @@ def run_b200(args, ws, rank, local):
     dist.barrier()
     # whole job: slowest rank's device time over the PCG iterations of ALL ranks
     # (replicas: every rank solves its own copy; N ranks do N x the iterations)
+    # replicas: value = the slowest rank's seconds per PCG iteration (each rank runs the
+    # same solve); the job's aggregate throughput is reported separately
     tot_ms = dist.max(tot_ms)
     job_it = dist.sum(float(tot_it))
-    value = (tot_ms / 1e3) / max(job_it, 1.0)
+    value = (tot_ms / 1e3) / max(tot_it, 1)
+    job_its_per_s = job_it / (tot_ms / 1e3) if tot_ms > 0 else None
     n_iters = per_solve[-1][1]
     converged = all(p[2] for p in per_solve)
 
@@ -333,7 +374,7 @@ def run_b200(args, ws, rank, local):
             e2e_t += dt
             e2e_it += int(n_it.value)
     e2e_t = dist.max(e2e_t)
-    e2e_value = e2e_t / max(dist.sum(float(e2e_it)), 1.0)
+    e2e_value = e2e_t / max(e2e_it, 1)
     x_host = np.ctypeslib.as_array(xp, shape=(n,)).copy()
     lib.aspamg_gpu_free_pinned(pin_b)
     lib.aspamg_gpu_free_pinned(pin_x)
@@ -352,13 +393,16 @@ def run_b200(args, ws, rank, local):
     k_ms, k_bytes = top[2], top[3]
     peak, peak_kind = measured_peak()
     achieved = k_bytes / (k_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_note = None, "no ncu capture of this kernel for this build"
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            traffic = tj.get(f"c{args.config}", {}).get(f"{top[0]}@L{top[1]}")
+            tag = kernel_build_tag()
+            ent = tj.get(tag, {}).get(f"c{args.config}", {}).get(f"{top[0]}@L{top[1]}")
+            if ent is not None:
+                traffic, traffic_note = ent, f"ncu --set full capture, build {tag} (profiles/traffic.json)"
         except Exception:
             traffic = None
 
@@ -372,6 +416,8 @@ def run_b200(args, ws, rank, local):
                "kind": "reference" if use_ref else "port",
                "sample": f"{iters} PCG iterations of this workload (same hierarchy), "
                          f"{'restated pcg/vcycle on the reference spmv (oracle/_ref)' if use_ref else 'oracle port'}"}
+        if not args.no_cpu_1t:
+            cpu["one_thread"] = cpu_one_thread(h, prob.rhs)
 
     dist.close()
     if rank != 0:
@@ -384,7 +430,7 @@ def run_b200(args, ws, rank, local):
         levels.append({"n": int(li.n), "nnz_A": int(li.a_nnz), "fmt": [fmts[int(f)] for f in li.fmt],
                        "fill": [round(float(f), 3) for f in li.fill], "omega": round(float(li.omega), 4)})
     line = {
-        "metric": "PCG+AMG solve: s/iteration (time-to-1e-8 = ms_per_step)",
+        "metric": METRIC,
         "value": value, "unit": "s/iteration", "higher_is_better": False,
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_ms / args.steps, "scaling": "weak", "vs_baseline": None,
@@ -393,13 +439,14 @@ def run_b200(args, ws, rank, local):
                    "levels": int(info.n_levels), "C_gd": info.C_gd, "C_op": info.C_op, "C_fs": info.C_fs,
                    "n_it": n_iters, "converged": converged, "true_rel_res": per_solve[-1][3],
                    "rel_tol": args.tol, "K_format": "bsr3" if lv0.a_format == 1 else "csr",
-                   "setup_s": t_setup, "setup_on": "cpu" if args.cpu_setup else "cpu + gpu (srqcg, galerkin)",
+                   "setup_s": t_setup, "setup_on": origin,
                    "upload_s": t_upload, "parallelism": f"replicas x{ws}",
                    "vcycle": "V(1,1), levels below the first with <= 1500 rows collapsed into one dense operator "
                              "formed on the device at upload (tail_dense); CSR long rows split to warp-per-row CTAs",
                    "l2": "inputs larger than L2 (K alone > 126 MB), no flush" if args.config != 1 else "K fits in L2"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": top[0], "level": top[1], "kernel_ms": k_ms,
+                     "traffic": traffic, "traffic_source": traffic_note, "kernel": top[0], "level": top[1],
+                     "kernel_ms": k_ms,
                      "alg_bytes": k_bytes, "peak_kind": peak_kind},
         "vcycle": {"ms": vc_ms, "alg_bytes": vc_bytes, "gbs": vc_bytes / (vc_ms * 1e-3) / 1e9 if vc_ms else None,
                    "frac": (vc_bytes / (vc_ms * 1e-3) / 1e9) / peak if vc_ms else None,
@@ -411,6 +458,7 @@ def run_b200(args, ws, rank, local):
                 "d2h_bytes_per_step": nbytes + 8 * n_iters},
         "levels": levels,
         "gpu_launches": launches,
+        "job_iterations_per_s": job_its_per_s,
         "clocks": clocks,
         "time_to_1e8_s": tot_ms / args.steps / 1e3,
     }
@@ -426,16 +474,16 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--scale", type=int, default=1)
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--max-it", dest="max_it", type=int, default=1000)
     ap.add_argument("--kernel-reps", dest="kernel_reps", type=int, default=20)
     ap.add_argument("--ref-sample-s", dest="ref_sample_s", type=float, default=12.0)
-    ap.add_argument("--full-iters", dest="full_iters", type=int, default=0)
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
+    ap.add_argument("--no-cpu-1t", dest="no_cpu_1t", action="store_true")
     ap.add_argument("--cpu-setup", dest="cpu_setup", action="store_true",
-                    help="run the whole setup on the CPU (default: SRQCG + Galerkin on the GPU, same hierarchy)")
+                    help="run the whole setup on the CPU (default: SRQCG, aFSAI and Galerkin on the GPU; the same hierarchy)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = dist_env()

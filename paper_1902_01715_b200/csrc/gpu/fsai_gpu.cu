@@ -4,14 +4,19 @@
 //
 // Restates csrc/host/fsai.cpp operation for operation, so G, omega and psi are
 // bit-identical to the host's:
-//   * afsai_build: one warp per row; the row's incremental Cholesky factor of
-//     A[P, P] (packed lower triangle), bordered solves and the gradient
-//     accumulator (open-addressing table keyed by column) live in shared
-//     memory. Every sum keeps the host order: dot4's four partial chains run on
-//     lanes 0..3 and combine as (s0 + s1) + (s2 + s3); the transposed solve's
-//     subtraction chain runs on lane 0 over products formed by all lanes; the
-//     gradient takes the pattern rows in insertion order, then row i. Candidate
-//     choice = the host's partial_sort order (|g| descending, column ascending).
+//   * afsai passes (fsai.cpp run_passes): one warp per row runs several
+//     refinement passes back to back (the factor is kept in the pattern's
+//     insertion order, so a pass continues exactly where the previous one
+//     stopped) and records the row of G after each pass. The row's incremental
+//     Cholesky factor of A[P, P] (packed; shared memory, or an L2-sized global
+//     scratch for long patterns), the bordered solves and the gradient
+//     accumulator (open addressing keyed by column) are per warp. The dense
+//     arithmetic is the lane-parallel order the host restates: dot products as
+//     32 strided partial sums + xor butterfly (dot_w32), the forward solve
+//     left-looking with dot_w32 rows, the transposed solve right-looking (lanes
+//     update b_k, k < i). The gradient takes the pattern rows in insertion order,
+//     then row i. Candidate choice = the host's partial_sort order (|g|
+//     descending, column ascending).
 //   * transpose: counting sort by column + per-column sort by row (the unique
 //     transpose, identical to core.cpp transpose()).
 //   * Lanczos: exact sequential CSR products (thread per row, ascending column
@@ -24,7 +29,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -37,21 +45,25 @@ constexpr unsigned FULL = 0xffffffffu;
 
 struct AfsaiArgs {
     DCsr64 A;
-    const long long* gs_rp = nullptr;  // start pattern (G of the previous pass) or null
+    const long long* gs_rp = nullptr;  // start pattern rows in insertion order (i itself skipped), or null
     const long long* gs_ci = nullptr;
-    int k = 0, rho = 0;
-    double eps = 0.0;
-    int mcap = 1, hcap = 1024;
+    int npass = 1;               // passes run back to back per row (fsai.cpp run_row)
+    int k0 = 0, rho0 = 0;        // pass 0
+    double eps0 = 0.0;
+    int ki = 0, rhoi = 0;        // passes 1 .. npass-1
+    double epsi = 0.0;
+    int mcap = 1, hcap = 1024;   // mcap: bound of the final pattern size
     int l_global = 0;            // factor in global scratch (rows too long for shared memory)
-    double* lscratch = nullptr;  // [gridDim.x * W][LP] when l_global
+    double* lscratch = nullptr;  // [gridDim.x * W][packed(mcap)] when l_global
     const long long* rows = nullptr;  // rows to process (null: all)
     long long nrows = 0;
-    int* cnt = nullptr;          // per row: m + 1 entries; -1 not SPD; -2 table overflow
-    long long* ocol = nullptr;   // n x (mcap + 1) scratch, row sorted by column
-    double* oval = nullptr;
-    long long* ocol_ins = nullptr;  // the same rows in insertion order (pattern, then i)
-    double* oval_ins = nullptr;
-    double* psi = nullptr;
+    // outputs: pass p of row i
+    int* cnt = nullptr;          // [npass][n]: m_p + 1 (row status in pass 0's slot: -1 not SPD, -2 table overflow)
+    double* psi = nullptr;       // [npass][n]
+    double* yout = nullptr;      // y_p[0..m_p) at yout + yoff[p] + i * ycap[p]
+    const long long* yoff = nullptr;
+    const int* ycap = nullptr;
+    int* pout = nullptr;         // final pattern, insertion order: pout + i * mcap
     unsigned long long* bad = nullptr;  // smallest failing row
 };
 
@@ -66,13 +78,13 @@ __host__ __device__ inline int pat_cap(int mcap) {
 
 __host__ __device__ inline size_t warp_bytes(int mcap, int hcap, bool l_global) {
     const size_t lp = l_global ? 0 : packed(mcap);
-    size_t b = 8 * (lp + 3 * (size_t)mcap + (size_t)hcap) +
+    size_t b = 8 * (lp + 2 * (size_t)mcap + (size_t)hcap) +
                4 * ((size_t)hcap + (size_t)mcap + 40 + 2 * (size_t)pat_cap(mcap));
     return (b + 15) & ~(size_t)15;
 }
 
 struct WarpMem {
-    double *L, *y, *a, *pr, *hv;
+    double *L, *y, *a, *hv;
     int *hk, *pat, *sel, *pk, *pv;
     int pcap;
 };
@@ -91,42 +103,34 @@ __device__ double a_at(const DCsr64& A, long long r, long long c) {
     return (lo < end && A.ci[lo] == c) ? A.v[lo] : 0.0;
 }
 
-// smalldense.cpp dot4 with its four partial chains on lanes 0..3; result on every lane.
-__device__ double dot4w(const double* x, const double* y, int n, int lane) {
+// smalldense.cpp dot_w32: lane l sums k = l, l+32, ... (separate mul / add), then
+// the xor butterfly; every lane ends with the same value (addition commutes).
+__device__ __forceinline__ double dot_w32(const double* x, const double* y, int n, int lane) {
     double s = 0.0;
-    const int n4 = n & ~3;
-    if (lane < 4) {
-#pragma unroll 4
-        for (int k = lane; k < n4; k += 4) s = __dadd_rn(s, __dmul_rn(x[k], y[k]));
-        if (lane == 0)
-            for (int k = n4; k < n; ++k) s = __dadd_rn(s, __dmul_rn(x[k], y[k]));
-    }
-    const double s1 = __shfl_sync(FULL, s, 1), s2 = __shfl_sync(FULL, s, 2), s3 = __shfl_sync(FULL, s, 3);
-    const double r = __dadd_rn(__dadd_rn(s, s1), __dadd_rn(s2, s3));
-    return __shfl_sync(FULL, r, 0);
+    for (int k = lane; k < n; k += 32) s = __dadd_rn(s, __dmul_rn(x[k], y[k]));
+#pragma unroll
+    for (int h = 16; h >= 1; h >>= 1) s = __dadd_rn(s, __shfl_xor_sync(FULL, s, h));
+    return s;
 }
 
-// smalldense.cpp trsv_lower on the packed factor (b may be the factor's row n).
+// smalldense.cpp trsv_lower (left-looking) on the packed factor (b may be the factor's row n).
 __device__ void trsv_lower_w(int n, const double* L, double* b, int lane) {
     for (int i = 0; i < n; ++i) {
         const double* Li = L + packed(i);
-        const double d = dot4w(Li, b, i, lane);
+        const double d = dot_w32(Li, b, i, lane);
         if (lane == 0) b[i] = __ddiv_rn(__dsub_rn(b[i], d), Li[i]);
         __syncwarp();
     }
 }
 
-// smalldense.cpp trsv_lower_t: s = b_i - L_{i+1,i} b_{i+1} - ... (sequential), products by all lanes.
-__device__ void trsv_lower_t_w(int n, const double* L, double* b, double* pr, int lane) {
+// smalldense.cpp trsv_lower_t (right-looking): b_i /= L_ii, then b_k -= L_ik b_i for k < i.
+__device__ void trsv_lower_t_w(int n, const double* L, double* b, int lane) {
     for (int i = n - 1; i >= 0; --i) {
-        for (int k = i + 1 + lane; k < n; k += 32) pr[k] = __dmul_rn(L[packed(k) + i], b[k]);
+        const double* Li = L + packed(i);
+        const double bi = __ddiv_rn(b[i], Li[i]);
         __syncwarp();
-        if (lane == 0) {
-            double s = b[i];
-#pragma unroll 4
-            for (int k = i + 1; k < n; ++k) s = __dsub_rn(s, pr[k]);
-            b[i] = __ddiv_rn(s, L[packed(i) + i]);
-        }
+        for (int k = lane; k < i; k += 32) b[k] = __dsub_rn(b[k], __dmul_rn(Li[k], bi));
+        if (lane == 0) b[i] = bi;
         __syncwarp();
     }
 }
@@ -185,7 +189,7 @@ __device__ bool chol_append_w(const DCsr64& A, const WarpMem& w, int m, long lon
     double* row = w.L + packed(m);
     const double ajj = gather_row(A, j, j, w, m, row, lane);
     trsv_lower_w(m, w.L, row, lane);
-    const double d = __dsub_rn(ajj, dot4w(row, row, m, lane));
+    const double d = __dsub_rn(ajj, dot_w32(row, row, m, lane));
     if (!(d > 0.0)) return false;
     if (lane == 0) row[m] = __dsqrt_rn(d);
     __syncwarp();
@@ -222,167 +226,169 @@ __device__ int h_find(const int* hk, int hcap, int key) {
     return -1;
 }
 
-// grad[j] += A(r, j) * gm for the j < i of row r (lanes take distinct j).
+// grad[j] += A(r, j) * gm for the j < i of row r (lanes take distinct j; the
+// row's columns ascend, so the entries past the first j >= i are skipped).
 __device__ void scatter_w(const DCsr64& A, long long r, double gm, long long i, const WarpMem& w, int hcap, int lane,
                           bool& ovf) {
     const long long b = A.rp[r], e = A.rp[r + 1];
-    for (long long q = b + lane; q < e; q += 32) {
-        const long long j = A.ci[q];
-        if (j >= i) continue;
-        const int slot = h_insert(w.hk, w.hv, hcap, (int)j, ovf);
-        if (slot >= 0) w.hv[slot] = __dadd_rn(w.hv[slot], __dmul_rn(A.v[q], gm));
+    for (long long q0 = b; q0 < e; q0 += 32) {
+        const long long q = q0 + lane;
+        const long long j = q < e ? A.ci[q] : LLONG_MAX;
+        if (j < i) {
+            const int slot = h_insert(w.hk, w.hv, hcap, (int)j, ovf);
+            if (slot >= 0) w.hv[slot] = __dadd_rn(w.hv[slot], __dmul_rn(A.v[q], gm));
+        }
+        if (__any_sync(FULL, j >= i)) break;
     }
     __syncwarp();
 }
 
-// One row of afsai_build (fsai.cpp:60-160).
+// One row of fsai.cpp run_row: npass passes back to back from the start pattern.
 __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int lane) {
     const DCsr64& A = P.A;
+    const long long n = A.n_rows;
     int m = 0;
-    bool ok = true;
     for (int q = lane; q < w.pcap; q += 32) w.pk[q] = -1;
     __syncwarp();
     if (P.gs_rp) {
         const long long b = P.gs_rp[i], e = P.gs_rp[i + 1];
         int ns = 0;
-        for (long long q = b + lane; q < e; q += 32) {
-            const long long c = P.gs_ci[q];
-            if (c < i) w.pat[q - b] = (int)c;
-        }
-        for (long long q0 = b; q0 < e; q0 += 32) {
-            const bool lt = q0 + lane < e && P.gs_ci[q0 + lane] < i;
-            ns += __popc(__ballot_sync(FULL, lt));
+        for (long long q0 = b; q0 < e; q0 += 32) {  // columns < i, in stored order
+            const long long c = q0 + lane < e ? P.gs_ci[q0 + lane] : LLONG_MAX;
+            const unsigned lt = __ballot_sync(FULL, c < i);
+            if (c < i) w.pat[ns + __popc(lt & ((1u << lane) - 1))] = (int)c;
+            ns += __popc(lt);
         }
         __syncwarp();
         for (int q = 0; q < ns; ++q) {
             if (lane == 0) pat_insert(w, w.pat[q], q);
             __syncwarp();
             if (!chol_append_w(A, w, m, w.pat[q], lane)) {
-                ok = false;
-                break;
+                if (lane == 0) {
+                    P.cnt[i] = -1;
+                    atomicMin(P.bad, (unsigned long long)i);
+                }
+                return;
             }
             ++m;
         }
     }
     double aii = lane == 0 ? a_at(A, i, i) : 0.0;
     aii = __shfl_sync(FULL, aii, 0);
-    double psi_prev = 0.0, psi = 0.0;
-    bool ovf = false;
-    for (int step = 0; ok; ++step) {
-        // bordered solve y = A_PP^{-1} a, psi = a_ii - a'y
-        gather_row(A, i, i, w, m, w.a, lane);
-        for (int q = lane; q < m; q += 32) w.y[q] = w.a[q];
-        __syncwarp();
-        trsv_lower_w(m, w.L, w.y, lane);
-        trsv_lower_t_w(m, w.L, w.y, w.pr, lane);
-        psi = __dsub_rn(aii, dot4w(w.a, w.y, m, lane));
-        if (!(psi > 0.0)) {
-            ok = false;
-            break;
-        }
-        if (step > 0 && __dsub_rn(psi_prev, psi) <= __dmul_rn(P.eps, psi_prev)) break;
-        if (step == P.k) break;
-        psi_prev = psi;
-        // gradient over the rows of P (insertion order) then row i
-        for (int s = lane; s < P.hcap; s += 32) w.hk[s] = -1;
-        __syncwarp();
-        for (int q = 0; q < m; ++q) scatter_w(A, w.pat[q], -w.y[q], i, w, P.hcap, lane, ovf);
-        scatter_w(A, i, 1.0, i, w, P.hcap, lane, ovf);
-        if (__any_sync(FULL, ovf)) {
-            ovf = true;
-            break;
-        }
-        for (int q = lane; q < m; q += 32) {  // exclude the pattern
-            const int sl = h_find(w.hk, P.hcap, w.pat[q]);
-            if (sl >= 0) w.hk[sl] = -2;
-        }
-        __syncwarp();
-        // the rho best candidates: |g| descending, then column ascending
-        int take = 0;
-        for (; take < P.rho; ++take) {
-            double bv = -1.0;
-            int bj = INT_MAX, bs = -1;
-            for (int s = lane; s < P.hcap; s += 32) {
-                const int key = w.hk[s];
-                if (key >= 0) {
-                    const double av = fabs(w.hv[s]);
-                    if (av > bv || (av == bv && key < bj)) {
-                        bv = av;
-                        bj = key;
-                        bs = s;
+    double psi = 0.0;
+    bool have = false;  // w.y / psi hold the bordered solve of the current pattern
+    for (int pass = 0; pass < P.npass; ++pass) {
+        const int k = pass ? P.ki : P.k0, rho = pass ? P.rhoi : P.rho0;
+        const double eps = pass ? P.epsi : P.eps0;
+        double psi_prev = 0.0;
+        for (int step = 0;; ++step) {
+            if (!have) {
+                // bordered solve y = A_PP^{-1} a, psi = a_ii - a'y
+                gather_row(A, i, i, w, m, w.a, lane);
+                for (int q = lane; q < m; q += 32) w.y[q] = w.a[q];
+                __syncwarp();
+                trsv_lower_w(m, w.L, w.y, lane);
+                trsv_lower_t_w(m, w.L, w.y, lane);
+                psi = __dsub_rn(aii, dot_w32(w.a, w.y, m, lane));
+                if (!(psi > 0.0)) {
+                    if (lane == 0) {
+                        P.cnt[i] = -1;
+                        atomicMin(P.bad, (unsigned long long)i);
+                    }
+                    return;
+                }
+                have = true;
+            }
+            if (step > 0 && __dsub_rn(psi_prev, psi) <= __dmul_rn(eps, psi_prev)) break;
+            if (step == k) break;
+            psi_prev = psi;
+            // gradient over the rows of P (insertion order) then row i
+            bool ovf = false;
+            for (int s = lane; s < P.hcap; s += 32) w.hk[s] = -1;
+            __syncwarp();
+            for (int q = 0; q < m; ++q) scatter_w(A, w.pat[q], -w.y[q], i, w, P.hcap, lane, ovf);
+            scatter_w(A, i, 1.0, i, w, P.hcap, lane, ovf);
+            if (__any_sync(FULL, ovf)) {
+                if (lane == 0) P.cnt[i] = -2;
+                return;
+            }
+            for (int q = lane; q < m; q += 32) {  // exclude the pattern
+                const int sl = h_find(w.hk, P.hcap, w.pat[q]);
+                if (sl >= 0) w.hk[sl] = -2;
+            }
+            __syncwarp();
+            // the rho best candidates: |g| descending, then column ascending
+            int take = 0;
+            for (; take < rho; ++take) {
+                double bv = -1.0;
+                int bj = INT_MAX, bs = -1;
+                for (int s = lane; s < P.hcap; s += 32) {
+                    const int key = w.hk[s];
+                    if (key >= 0) {
+                        const double av = fabs(w.hv[s]);
+                        if (av > bv || (av == bv && key < bj)) {
+                            bv = av;
+                            bj = key;
+                            bs = s;
+                        }
                     }
                 }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_down_sync(FULL, bv, o);
-                const int oj = __shfl_down_sync(FULL, bj, o), os = __shfl_down_sync(FULL, bs, o);
-                if (ov > bv || (ov == bv && oj < bj)) {
-                    bv = ov;
-                    bj = oj;
-                    bs = os;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_down_sync(FULL, bv, o);
+                    const int oj = __shfl_down_sync(FULL, bj, o), os = __shfl_down_sync(FULL, bs, o);
+                    if (ov > bv || (ov == bv && oj < bj)) {
+                        bv = ov;
+                        bj = oj;
+                        bs = os;
+                    }
                 }
-            }
-            bs = __shfl_sync(FULL, bs, 0);
-            bj = __shfl_sync(FULL, bj, 0);
-            if (bs < 0) break;
-            if (lane == 0) {
-                w.sel[take] = bj;
-                w.hk[bs] = -2;
-            }
-            __syncwarp();
-        }
-        if (take == 0) break;
-        if (lane == 0)  // ascending column order of the chosen candidates
-            for (int a = 1; a < take; ++a) {
-                const int v = w.sel[a];
-                int b = a - 1;
-                while (b >= 0 && w.sel[b] > v) {
-                    w.sel[b + 1] = w.sel[b];
-                    --b;
+                bs = __shfl_sync(FULL, bs, 0);
+                bj = __shfl_sync(FULL, bj, 0);
+                if (bs < 0) break;
+                if (lane == 0) {
+                    w.sel[take] = bj;
+                    w.hk[bs] = -2;
                 }
-                w.sel[b + 1] = v;
+                __syncwarp();
             }
-        __syncwarp();
-        for (int c = 0; c < take && ok; ++c) {
-            const int j = w.sel[c];
-            if (lane == 0) {
-                w.pat[m] = j;
-                pat_insert(w, j, m);
-            }
+            if (take == 0) break;
+            if (lane == 0)  // ascending column order of the chosen candidates
+                for (int a = 1; a < take; ++a) {
+                    const int v = w.sel[a];
+                    int b = a - 1;
+                    while (b >= 0 && w.sel[b] > v) {
+                        w.sel[b + 1] = w.sel[b];
+                        --b;
+                    }
+                    w.sel[b + 1] = v;
+                }
             __syncwarp();
-            if (!chol_append_w(A, w, m, j, lane)) ok = false;
-            else ++m;
+            for (int c = 0; c < take; ++c) {
+                const int j = w.sel[c];
+                if (lane == 0) {
+                    w.pat[m] = j;
+                    pat_insert(w, j, m);
+                }
+                __syncwarp();
+                if (!chol_append_w(A, w, m, j, lane)) {
+                    if (lane == 0) {
+                        P.cnt[i] = -1;
+                        atomicMin(P.bad, (unsigned long long)i);
+                    }
+                    return;
+                }
+                ++m;
+            }
+            have = false;
         }
-    }
-    if (!ok) {
+        double* yo = P.yout + P.yoff[pass] + i * (long long)P.ycap[pass];
+        for (int q = lane; q < m; q += 32) yo[q] = w.y[q];
         if (lane == 0) {
-            P.cnt[i] = -1;
-            atomicMin(P.bad, (unsigned long long)i);
+            P.cnt[pass * n + i] = m + 1;
+            P.psi[pass * n + i] = psi;
         }
-        return;
     }
-    if (ovf) {
-        if (lane == 0) P.cnt[i] = -2;
-        return;
-    }
-    // row = (-y, 1) / sqrt(psi), columns ascending
-    const double s = __ddiv_rn(1.0, __dsqrt_rn(psi));
-    const long long base = i * (long long)(P.mcap + 1);
-    for (int e = lane; e <= m; e += 32) {
-        const long long col = e < m ? (long long)w.pat[e] : i;
-        const double val = e < m ? __dmul_rn(-w.y[e], s) : s;
-        int rank = 0;
-        for (int f = 0; f < m; ++f) rank += (long long)w.pat[f] < col;
-        if (e < m) rank += i < col;
-        P.ocol[base + rank] = col;
-        P.oval[base + rank] = val;
-        P.ocol_ins[base + e] = col;
-        P.oval_ins[base + e] = val;
-    }
-    if (lane == 0) {
-        P.cnt[i] = m + 1;
-        P.psi[i] = psi;
-    }
+    for (int q = lane; q < m; q += 32) P.pout[i * (long long)P.mcap + q] = w.pat[q];
     __syncwarp();
 }
 
@@ -399,8 +405,7 @@ __global__ void k_afsai(const AfsaiArgs P) {
     }
     w.y = reinterpret_cast<double*>(p);
     w.a = w.y + P.mcap;
-    w.pr = w.a + P.mcap;
-    w.hv = w.pr + P.mcap;
+    w.hv = w.a + P.mcap;
     w.hk = reinterpret_cast<int*>(w.hv + P.hcap);
     w.pat = w.hk + P.hcap;
     w.sel = w.pat + P.mcap;
@@ -412,16 +417,32 @@ __global__ void k_afsai(const AfsaiArgs P) {
         afsai_row(P, w, P.rows ? P.rows[t] : t, lane);
 }
 
-// rows of the scratch -> CSR (warp per row)
-__global__ void k_compact(long long n, const long long* __restrict__ rp, int rowcap, const long long* __restrict__ ocol,
-                          const double* __restrict__ oval, long long* ci, double* v) {
+// Pass p of a batch -> G_p (rows sorted by column) and its insertion-ordered twin
+// (pattern, then i) — fsai.cpp pass_matrix. Warp per row.
+__global__ void k_pass_csr(long long n, const long long* __restrict__ rp, const int* __restrict__ cnt,
+                           const double* __restrict__ psi, const double* __restrict__ y, int ycap,
+                           const int* __restrict__ pout, int mcap, long long* ci, double* v, long long* ici,
+                           double* iv) {
     const int lane = threadIdx.x & 31;
     const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
-        const long long b = rp[i], len = rp[i + 1] - b, src = i * (long long)rowcap;
-        for (long long q = lane; q < len; q += 32) {
-            ci[b + q] = ocol[src + q];
-            v[b + q] = oval[src + q];
+        const int m = cnt[i] - 1;
+        const double s = __ddiv_rn(1.0, __dsqrt_rn(psi[i]));
+        const int* pt = pout + i * (long long)mcap;
+        const double* yi = y + i * (long long)ycap;
+        const long long b = rp[i];
+        for (int e = lane; e <= m; e += 32) {
+            const long long col = e < m ? (long long)pt[e] : i;
+            const double val = e < m ? __dmul_rn(-yi[e], s) : s;
+            int rank = m;  // i closes the row (pattern columns are < i)
+            if (e < m) {
+                rank = 0;
+                for (int f = 0; f < m; ++f) rank += pt[f] < pt[e];
+            }
+            ci[b + rank] = col;
+            v[b + rank] = val;
+            ici[b + e] = col;
+            iv[b + e] = val;
         }
     }
 }
@@ -504,23 +525,82 @@ int sm_count() {
     return sms;
 }
 
-// afsai_build on the device; A device-resident, start pattern optional.
-DevG afsai_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const DevG* Gs, int k, int rho, double eps,
-                  double* psi) {
+// fsai.cpp run_passes on the device: npass passes of every row, back to back,
+// from the insertion-ordered start pattern (null = identity start).
+struct PassParams {
+    int k, rho;
+    double eps;
+};
+struct Batch {
+    long long n = 0;
+    int npass = 0, mcap = 1;
+    int* cnt = nullptr;
+    double* psi = nullptr;
+    double* y = nullptr;
+    int* pout = nullptr;
+    long long* d_yoff = nullptr;
+    int* d_ycap = nullptr;
+    std::vector<long long> yoff;
+    std::vector<int> ycap;
+};
+
+void free_batch(aspamg_gpu_ctx* c, Batch& b) {
+    dfree(c, b.cnt);
+    dfree(c, b.psi);
+    dfree(c, b.y);
+    dfree(c, b.pout);
+    dfree(c, b.d_yoff);
+    dfree(c, b.d_ycap);
+    b = Batch{};
+}
+
+constexpr int kMaxPattern = 4096;
+
+long long max_row(const DevG* g) {
+    long long r = 0;
+    if (g)
+        for (size_t i = 0; i + 1 < g->rp.size(); ++i) r = std::max(r, g->rp[i + 1] - g->rp[i]);
+    return r;
+}
+
+// device bytes of a batch of npass passes (yout + pattern + counters)
+double batch_bytes(long long n, long long gs_max, int npass, const PassParams& p0, const PassParams& pr) {
+    double ys = 0.0;
+    long long cap = gs_max + (long long)p0.k * p0.rho;
+    for (int p = 0; p < npass; ++p) {
+        if (p) cap += (long long)pr.k * pr.rho;
+        ys += double(cap);
+    }
+    return double(n) * (8.0 * ys + 4.0 * double(cap) + 12.0 * npass);
+}
+
+Batch run_passes_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const DevG* Gs, int npass,
+                        const PassParams& p0, const PassParams& pr) {
     cudaStream_t s = c->stream;
     const long long n = A.n_rows;
-    long long gs_max = 0;
-    if (Gs)
-        for (long long i = 0; i < n; ++i) gs_max = std::max(gs_max, Gs->rp[(size_t)i + 1] - Gs->rp[(size_t)i]);
-    const long long mcap_ll = gs_max + (long long)k * rho + 1;
-    if (mcap_ll > 4096) throw Fail{4, "afsai (GPU): pattern bound exceeds 4096 entries per row"};
-    const int mcap = (int)mcap_ll;
-    const int rowcap = mcap + 1;
-    int* cnt = dalloc<int>(c, (size_t)std::max<long long>(n, 1));
-    long long* ocol = dalloc<long long>(c, (size_t)std::max<long long>(n, 1) * rowcap);
-    double* oval = dalloc<double>(c, (size_t)std::max<long long>(n, 1) * rowcap);
-    long long* ocol_ins = dalloc<long long>(c, (size_t)std::max<long long>(n, 1) * rowcap);
-    double* oval_ins = dalloc<double>(c, (size_t)std::max<long long>(n, 1) * rowcap);
+    const long long gs_max = max_row(Gs);  // includes the diagonal: a bound of the start pattern
+    Batch B;
+    B.n = n;
+    B.npass = npass;
+    long long cap = gs_max + (long long)p0.k * p0.rho, tot = 0;
+    for (int p = 0; p < npass; ++p) {
+        if (p) cap += (long long)pr.k * pr.rho;
+        B.ycap.push_back((int)std::max<long long>(cap, 1));
+        B.yoff.push_back(tot);
+        tot += (long long)B.ycap.back() * std::max<long long>(n, 1);
+    }
+    if (cap > kMaxPattern) throw Fail{4, "afsai (GPU): pattern bound exceeds 4096 entries per row"};
+    B.mcap = (int)std::max<long long>(cap, 1);
+    const int mcap = B.mcap;
+    const size_t nn = (size_t)std::max<long long>(n, 1);
+    B.cnt = dalloc<int>(c, nn * npass);
+    B.psi = dalloc<double>(c, nn * npass);
+    B.y = dalloc<double>(c, (size_t)std::max<long long>(tot, 1));
+    B.pout = dalloc<int>(c, nn * mcap);
+    B.d_yoff = dalloc<long long>(c, (size_t)npass);
+    B.d_ycap = dalloc<int>(c, (size_t)npass);
+    CK(cudaMemcpyAsync(B.d_yoff, B.yoff.data(), 8 * (size_t)npass, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(B.d_ycap, B.ycap.data(), 4 * (size_t)npass, cudaMemcpyHostToDevice, s));
     unsigned long long* bad = dalloc<unsigned long long>(c, 1);
     const unsigned long long none = ~0ull;
     CK(cudaMemcpyAsync(bad, &none, 8, cudaMemcpyHostToDevice, s));
@@ -531,37 +611,47 @@ DevG afsai_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const 
     // table sizes: an upper bound of the touched columns, capped; overflowing rows rerun wider
     const long long touch = (long long)(mcap + 1) * std::max<long long>(a_maxrow, 1);
     int hcap = 64;
-    while (hcap < touch && hcap < 1024) hcap <<= 1;
-    for (int attempt = 0; attempt < 3; ++attempt) {
+    while (hcap < touch && hcap < 2048) hcap <<= 1;
+    for (int attempt = 0; attempt < 4; ++attempt) {
         AfsaiArgs P;
         P.A = A;
         P.gs_rp = Gs ? Gs->d.rp : nullptr;
         P.gs_ci = Gs ? Gs->ins.ci : nullptr;  // factor order = insertion order (fsai.cpp run_row)
-        P.k = k;
-        P.rho = rho;
-        P.eps = eps;
+        P.npass = npass;
+        P.k0 = p0.k;
+        P.rho0 = p0.rho;
+        P.eps0 = p0.eps;
+        P.ki = pr.k;
+        P.rhoi = pr.rho;
+        P.epsi = pr.eps;
         P.mcap = mcap;
         P.hcap = hcap;
-        P.cnt = cnt;
-        P.ocol = ocol;
-        P.oval = oval;
-        P.ocol_ins = ocol_ins;
-        P.oval_ins = oval_ins;
-        P.psi = psi;
+        P.cnt = B.cnt;
+        P.psi = B.psi;
+        P.yout = B.y;
+        P.yoff = B.d_yoff;
+        P.ycap = B.d_ycap;
+        P.pout = B.pout;
         P.bad = bad;
-        long long* drows = nullptr;
         if (attempt > 0) {
-            drows = dalloc<long long>(c, todo.size());
+            long long* drows = dalloc<long long>(c, todo.size());
             scratch.push_back(drows);
             CK(cudaMemcpyAsync(drows, todo.data(), todo.size() * 8, cudaMemcpyHostToDevice, s));
             P.rows = drows;
             P.nrows = (long long)todo.size();
         }
+        // rows in flight: the factor in shared memory while it fits, else in a global
+        // scratch sized to stay L2-resident (a few warps per SM)
         const size_t budget = 200 * 1024;
-        bool lg = warp_bytes(mcap, hcap, false) > budget;
+        const bool lg = warp_bytes(mcap, hcap, false) > budget;
         const size_t wb = warp_bytes(mcap, hcap, lg);
         if (wb > budget) throw Fail{4, "afsai (GPU): row workspace exceeds shared memory"};
-        const int W = (int)std::max<size_t>(1, std::min<size_t>(16, budget / wb));
+        int W = (int)std::max<size_t>(1, std::min<size_t>(16, budget / wb));
+        if (lg) {
+            const double per_warp = 8.0 * double(packed(mcap));
+            const int w_l2 = (int)std::max(1.0, 96e6 / (per_warp * sms));  // factors of all warps ~ 96 MB
+            W = std::max(1, std::min(W, w_l2));
+        }
         const size_t smem = wb * W;
         CK(cudaFuncSetAttribute(k_afsai, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 1;
@@ -578,19 +668,33 @@ DevG afsai_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const 
             k_afsai<<<grid, 32 * W, smem, s>>>(P);
             CK(cudaGetLastError());
         }
-        CK(cudaMemcpyAsync(hc.data(), cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hc.data(), B.cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         todo.clear();
         for (long long i = 0; i < n; ++i)
             if (hc[(size_t)i] == -2) todo.push_back(i);
         if (todo.empty()) break;
-        hcap = attempt == 0 ? 4096 : 16384;
+        hcap = attempt == 0 ? 4096 : attempt == 1 ? 8192 : 16384;
     }
     if (!todo.empty()) throw Fail{4, "afsai (GPU): gradient support exceeds 16384 columns in a row"};
     unsigned long long hbad = 0;
     CK(cudaMemcpy(&hbad, bad, 8, cudaMemcpyDeviceToHost));
-    if (hbad != none)
+    for (void* q : scratch) dfree(c, q);
+    dfree(c, bad);
+    if (hbad != none) {
+        free_batch(c, B);
         throw Fail{2, "afsai_build: non-positive local pivot at row " + std::to_string((long long)hbad)};
+    }
+    return B;
+}
+
+// Pass p of a batch as a device CSR (sorted) + its insertion-ordered twin; psi_p -> psi.
+DevG pass_device(aspamg_gpu_ctx* c, const Batch& B, int p, double* psi) {
+    cudaStream_t s = c->stream;
+    const long long n = B.n;
+    std::vector<int> hc((size_t)n);
+    CK(cudaMemcpyAsync(hc.data(), B.cnt + (size_t)p * n, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     DevG G;
     G.rp.assign((size_t)n + 1, 0);
     for (long long i = 0; i < n; ++i) G.rp[(size_t)i + 1] = G.rp[(size_t)i] + hc[(size_t)i];
@@ -598,20 +702,17 @@ DevG afsai_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const 
     G.d.rp = dalloc<long long>(c, (size_t)n + 1);
     G.d.ci = dalloc<long long>(c, (size_t)std::max<long long>(nnz, 1));
     G.d.v = dalloc<double>(c, (size_t)std::max<long long>(nnz, 1));
-    CK(cudaMemcpyAsync(G.d.rp, G.rp.data(), G.rp.size() * 8, cudaMemcpyHostToDevice, s));
     G.ins.ci = dalloc<long long>(c, (size_t)std::max<long long>(nnz, 1));
     G.ins.v = dalloc<double>(c, (size_t)std::max<long long>(nnz, 1));
-    k_compact<<<sms * 8, 256, 0, s>>>(n, G.d.rp, rowcap, ocol, oval, G.d.ci, G.d.v);
-    k_compact<<<sms * 8, 256, 0, s>>>(n, G.d.rp, rowcap, ocol_ins, oval_ins, G.ins.ci, G.ins.v);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(s));
-    for (void* q : scratch) dfree(c, q);
-    dfree(c, cnt);
-    dfree(c, ocol);
-    dfree(c, oval);
-    dfree(c, ocol_ins);
-    dfree(c, oval_ins);
-    dfree(c, bad);
+    CK(cudaMemcpyAsync(G.d.rp, G.rp.data(), G.rp.size() * 8, cudaMemcpyHostToDevice, s));
+    if (n > 0) {
+        k_pass_csr<<<sm_count() * 8, 256, 0, s>>>(n, G.d.rp, B.cnt + (size_t)p * n, B.psi + (size_t)p * n,
+                                                  B.y + B.yoff[(size_t)p], B.ycap[(size_t)p], B.pout, B.mcap,
+                                                  G.d.ci, G.d.v, G.ins.ci, G.ins.v);
+        CK(cudaGetLastError());
+    }
+    if (psi) CK(cudaMemcpyAsync(psi, B.psi + (size_t)p * n, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));  // G.rp (host) outlives the copy
     G.d.view = {n, n, nnz, G.d.rp, G.d.ci, G.d.v};
     G.ins.view = {n, n, nnz, G.d.rp, G.ins.ci, G.ins.v};
     return G;
@@ -686,18 +787,25 @@ double lanczos_device(DevLA& E, const DCsr64& G, const DCsr64& Gt, const DCsr64&
     return 1.05 * ev[(size_t)m - 1];
 }
 
-// Level policy (measured, profiles/setup_timing_*.json). The exact per-row
-// restatement keeps each row's factor (m(m+1)/2 doubles) and gradient table on
-// chip, so rows in flight per SM fall as m^2 and every append walks an A row:
-//  * operators with mean rows above smoother_max_mean_row (the dense coarse
-//    Galerkin levels) or fewer than smoother_min_rows rows are declined
-//    (status -1): the host computes them;
-//  * refinement passes whose pattern bound would exceed smoother_max_pattern
-//    are handed back (status -2, state after the last finished pass): the host
-//    continues the same loop from there — bit-identical either way.
-double g_smoother_max_mean_row = 300.0;
-double g_smoother_min_rows = 50000.0;
-double g_smoother_max_pattern = 64.0;
+// Level policy: operators with fewer than smoother_min_rows rows, or mean rows
+// above smoother_max_mean_row (0 = no bound), are declined (status -1: the host
+// computes them — small levels are latency-bound on the device); a refinement
+// batch whose pattern bound would exceed smoother_max_pattern (0 = only the
+// kernel's 4096 limit) is handed back (status -2, state after the last finished
+// pass): the host continues the same loop from there — bit-identical either way.
+double g_smoother_max_mean_row = 0.0;
+double g_smoother_min_rows = 20000.0;
+double g_smoother_max_pattern = 0.0;
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+double device_free_bytes() {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 8e9;
+    return double(fr);
+}
 
 }  // namespace
 }  // namespace aspamg_gpu
@@ -722,9 +830,11 @@ extern "C" int aspamg_gpu_set_setup_policy(const char* key, double value) {
     return 4;
 }
 
-// fsai.cpp smoother_setup (Alg. 3) on the device. A: host view; G written through
-// alloc(sink, ...); psi[n] (host) receives the final pass's Schur complements
-// (the host forms the Kaporin estimate from them).
+// fsai.cpp smoother_setup (Alg. 3) on the device, batched exactly as the host's:
+// passes computed back to back per row (run_passes_device), consumed one at a
+// time (Lanczos, omega, loop guards). A: host view; G written through alloc(sink,
+// ...); psi[n] (host) receives the final pass's Schur complements (the host forms
+// the Kaporin estimate from them).
 extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A, const aspamg_smoother_params* prm,
                                          aspamg_csr_alloc_fn alloc, void* sink, double* psi_out, double* omega,
                                          double* lambda_hat, int64_t* passes, int* exit_reason) {
@@ -757,24 +867,63 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
             if (!(lam > 0.0)) throw Fail{4, "compute_omega: lambda_hat must be positive"};
             return std::min(1.0, 2.0 / lam);
         };
-        DevG G = afsai_device(c, dA.view, a_maxrow, nullptr, (int)prm->k0, (int)prm->rho0, prm->eps0, psi);
+        const PassParams p0{(int)prm->k0, (int)prm->rho0, prm->eps0}, pr{(int)prm->ki, (int)prm->rhoi, prm->epsi};
+        Batch B;
+        int next = 0, last_batch = 1;
+        std::vector<double> lam_hist, nnzr_hist;
+        const bool trace = std::getenv("ASPAMG_SETUP_TRACE") != nullptr;
+        DevG G;
+        // next pass from the batch (a new batch when the current one is used up);
+        // false: the batch's pattern bound exceeds the policy -> hand back
+        auto take = [&](bool first, DevG& out, double* ps) -> bool {
+            if (next >= B.npass) {
+                free_batch(c, B);
+                const long long gs_max = first ? 0 : max_row(&G);
+                int want = first ? 1 : 2 * last_batch;
+                const size_t h = lam_hist.size();
+                if (!first && h >= 2) {  // fsai.cpp take_pass: predicted remaining passes
+                    const double dl = lam_hist[h - 2] - lam_hist[h - 1];
+                    const double dz = nnzr_hist[h - 1] - nnzr_hist[h - 2];
+                    double pred = 1e9;
+                    if (dl > 0) pred = std::min(pred, (lam_hist[h - 1] - 2.0 / prm->omega_bar) / dl);
+                    if (dz > 0) pred = std::min(pred, (prm->rho_bar - nnzr_hist[h - 1]) / dz);
+                    if (pred < 1e9) want = std::min(want, (int)std::ceil(std::max(pred, 0.0)) + 1);
+                }
+                want = std::max(1, std::min(want, 16));
+                const double budget = 0.5 * device_free_bytes();
+                while (want > 1 && batch_bytes(n, gs_max, want, first ? p0 : pr, pr) > budget) --want;
+                if (!first) {
+                    const long long bound = gs_max + (long long)want * pr.k * pr.rho;
+                    if ((g_smoother_max_pattern > 0 && double(gs_max + (long long)pr.k * pr.rho) > g_smoother_max_pattern) ||
+                        gs_max + (long long)pr.k * pr.rho > kMaxPattern)
+                        return false;
+                    while (want > 1 && gs_max + (long long)want * pr.k * pr.rho > kMaxPattern) --want;
+                    (void)bound;
+                }
+                last_batch = want;
+                const double t0 = now_s();
+                B = run_passes_device(c, dA.view, a_maxrow, first ? nullptr : &G, want, first ? p0 : pr, pr);
+                next = 0;
+                if (trace)
+                    std::fprintf(stderr, "[gpu smoother n=%lld] batch of %d passes: %.2f s\n", n, want, now_s() - t0);
+            }
+            out = pass_device(c, B, next++, ps);
+            return true;
+        };
+        take(true, G, psi);
         DevCsr Gt = transpose_device(c, G);
         double lam = lanczos_device(E, G.d.view, Gt.view, dA.view, prm->lanczos_steps, prm->seed, v, vp, w, t1, t2);
         double om = omega_of(lam);
         int64_t np = 0;
         int ex = 0;  // omega_reached
         while (om < prm->omega_bar) {
-            if (g_smoother_max_pattern > 0) {  // hand the remaining passes to the host?
-                long long gmax = 0;
-                for (long long i = 0; i < n; ++i) gmax = std::max(gmax, G.rp[(size_t)i + 1] - G.rp[(size_t)i]);
-                if (double(gmax + prm->ki * prm->rhoi + 1) > g_smoother_max_pattern) {
-                    handed = true;
-                    break;
-                }
-            }
             const double nnz_r = n ? double(G.d.view.nnz) / double(n) : 0.0;
             if (!(nnz_r < prm->rho_bar)) { ex = 1; break; }  // density_bound
-            DevG G2 = afsai_device(c, dA.view, a_maxrow, &G, (int)prm->ki, (int)prm->rhoi, prm->epsi, psi2);
+            DevG G2;
+            if (!take(false, G2, psi2)) {
+                handed = true;
+                break;
+            }
             if (G2.d.view.nnz == G.d.view.nnz) {  // pattern_stagnation
                 free_g(c, G2);
                 ex = 2;
@@ -787,9 +936,12 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
             Gt = transpose_device(c, G);
             lam = lanczos_device(E, G.d.view, Gt.view, dA.view, prm->lanczos_steps, prm->seed, v, vp, w, t1, t2);
             om = omega_of(lam);
+            lam_hist.push_back(lam);
+            nnzr_hist.push_back(n ? double(G.d.view.nnz) / double(n) : 0.0);
             ++np;
             ex = 0;
         }
+        free_batch(c, B);
         int64_t *rp = nullptr, *ci = nullptr;
         double* vals = nullptr;
         const long long nnz = G.d.view.nnz;
@@ -827,7 +979,10 @@ extern "C" int aspamg_gpu_afsai_build(void* device, const aspamg_csr_view* A, in
         for (long long i = 0; i < n; ++i) a_maxrow = std::max<long long>(a_maxrow, A->row_offsets[i + 1] - A->row_offsets[i]);
         const DevCsr dA = upload64(c, *A);
         double* psi = dalloc<double>(c, (size_t)std::max<long long>(n, 1));
-        DevG G = afsai_device(c, dA.view, a_maxrow, nullptr, (int)k, (int)rho, eps, psi);
+        const PassParams pp{(int)k, (int)rho, eps};
+        Batch B = run_passes_device(c, dA.view, a_maxrow, nullptr, 1, pp, pp);
+        DevG G = pass_device(c, B, 0, psi);
+        free_batch(c, B);
         int64_t *rp = nullptr, *ci = nullptr;
         double* vals = nullptr;
         const long long nnz = G.d.view.nnz;

@@ -57,7 +57,7 @@ bool chol_append(const Csr& A, RowWork& w, const std::vector<index_t>& pat, int 
     for (index_t k = A.row_begin(j); k < A.row_end(j); ++k)
         w.dense[static_cast<size_t>(A.col[static_cast<size_t>(k)])] = 0.0;
     trsv_lower(m, w.L.data(), w.cap, row);
-    const double d = ajj - dot_fixed4(row, row, m);
+    const double d = ajj - dot_w32(row, row, m);
     if (!(d > 0.0)) return false;
     row[m] = std::sqrt(d);
     return true;
@@ -138,7 +138,7 @@ bool run_row(const Csr& A, RowWork& w, index_t i, const index_t* st, index_t ns,
                 a.assign(y.begin(), y.end());
                 trsv_lower(m, w.L.data(), w.cap, y.data());
                 trsv_lower_t(m, w.L.data(), w.cap, y.data());
-                psi = aii - dot_fixed4(a.data(), y.data(), m);
+                psi = aii - dot_w32(a.data(), y.data(), m);
                 if (!(psi > 0.0)) return false;
                 have = true;
             }

@@ -23,33 +23,35 @@ long cholesky_lower(int n, double* a) {
     return -1;
 }
 
-// Four independent partial sums (fixed order, combined pairwise) break the
-// dependent add chain of the row dot product: same result for every run and
-// thread count, ~4x the throughput of a single accumulator.
-static inline double dot4(const double* a, const double* b, int n) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+// 32 strided partial sums — partial l takes k = l, l + 32, ... in ascending
+// order, each term a separate multiply and add — combined by the xor butterfly
+// (16, 8, 4, 2, 1) that a warp's __shfl_xor_sync reduction performs; lane 0's
+// value is the result. The device aFSAI kernel (fsai_gpu.cu dot_w32) runs the
+// identical sequence, so both produce the same bits.
+double dot_w32(const double* a, const double* b, int n) {
+    double s[32];
+    for (int l = 0; l < 32; ++l) s[l] = 0.0;
     int k = 0;
-    for (; k + 4 <= n; k += 4) {
-        s0 += a[k] * b[k];
-        s1 += a[k + 1] * b[k + 1];
-        s2 += a[k + 2] * b[k + 2];
-        s3 += a[k + 3] * b[k + 3];
-    }
-    for (; k < n; ++k) s0 += a[k] * b[k];
-    return (s0 + s1) + (s2 + s3);
+    for (; k + 32 <= n; k += 32)
+        for (int l = 0; l < 32; ++l) s[l] += a[k + l] * b[k + l];
+    for (int l = 0; k + l < n; ++l) s[l] += a[k + l] * b[k + l];
+    for (int h = 16; h >= 1; h >>= 1)  // lanes < h keep s_l + s_{l xor h} (= s_l + s_{l+h})
+        for (int l = 0; l < h; ++l) s[l] = s[l] + s[l + h];
+    return s[0];
 }
 
-double dot_fixed4(const double* a, const double* b, int n) { return dot4(a, b, n); }
-
+// Left-looking: b_i = (b_i - dot_w32(L_i, b, i)) / L_ii.
 void trsv_lower(int n, const double* L, int ld, double* b) {
-    for (int i = 0; i < n; ++i) b[i] = (b[i] - dot4(L + (size_t)i * ld, b, i)) / L[i * ld + i];
+    for (int i = 0; i < n; ++i) b[i] = (b[i] - dot_w32(L + (size_t)i * ld, b, i)) / L[(size_t)i * ld + i];
 }
 
+// Right-looking: b_i /= L_ii, then b_k -= L_ik b_i for k < i (i descending).
 void trsv_lower_t(int n, const double* L, int ld, double* b) {
     for (int i = n - 1; i >= 0; --i) {
-        double s = b[i];
-        for (int k = i + 1; k < n; ++k) s -= L[k * ld + i] * b[k];
-        b[i] = s / L[i * ld + i];
+        const double* Li = L + (size_t)i * ld;
+        const double bi = b[i] / Li[i];
+        b[i] = bi;
+        for (int k = 0; k < i; ++k) b[k] = b[k] - Li[k] * bi;
     }
 }
 

@@ -11,11 +11,13 @@ namespace aspamg {
 // the first non-positive pivot, or -1 on success. The strict upper part is
 // zeroed.
 long cholesky_lower(int n, double* a);
-// sum_k a[k] b[k] with four fixed partial sums (deterministic).
-double dot_fixed4(const double* a, const double* b, int n);
-// Solve L y = b in place (L row-major lower, leading dimension ld).
+// sum_k a[k] b[k] in the order of a 32-lane warp reduction: 32 strided partial
+// sums combined by the xor butterfly (deterministic; the device aFSAI's order).
+double dot_w32(const double* a, const double* b, int n);
+// Solve L y = b in place (L row-major lower, leading dimension ld), left-looking
+// with dot_w32 row products.
 void trsv_lower(int n, const double* L, int ld, double* b);
-// Solve L' y = b in place.
+// Solve L' y = b in place, right-looking (b_k -= L_ik b_i, i descending).
 void trsv_lower_t(int n, const double* L, int ld, double* b);
 
 // Symmetric eigen-decomposition by cyclic Jacobi. `a` (row-major n x n) is

@@ -56,9 +56,9 @@ def _all_gpu(pkg):
 
 
 def _default_policy(pkg):
-    pkg.gpu_setup_policy("smoother_max_mean_row", 300)
-    pkg.gpu_setup_policy("smoother_min_rows", 50000)
-    pkg.gpu_setup_policy("smoother_max_pattern", 64)
+    pkg.gpu_setup_policy("smoother_max_mean_row", 0)
+    pkg.gpu_setup_policy("smoother_min_rows", 20000)
+    pkg.gpu_setup_policy("smoother_max_pattern", 0)
 
 
 def test_srqcg_backend_hook_cpu(pkg):

@@ -29,13 +29,14 @@ def _worker(rank, ws, port, cache_root, q):
     import paper_1902_01715_b200 as P
     bench.ROOT = cache_root  # private cache dir for the test
     d = bench.Dist(ws, rank, rank, "gloo")
-    prob, h, t_gen, t_setup = bench.get_hierarchy(P, 1, 4, rank, d, 2)
+    prob, h, t_gen, t_setup, origin = bench.get_hierarchy(P, 1, 4, rank, d, 2)
     lv = h.level(1)
     chk = float(np.sum(lv.A.values)) + float(np.sum(h.level(0).G.values))
     import pyoracle as O
     st, x, hist, conv, trr = O.OracleHierarchy(h).pcg(prob.rhs)
     t = d.max(float(rank + 1))
     tot = d.sum(float(len(hist)))
+    assert origin == ("cpu" if rank == 0 else "cached: cpu")
     q.put((rank, chk, len(hist), conv, t, tot))
     d.close()
 

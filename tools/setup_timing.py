@@ -34,7 +34,7 @@ def main():
     ap.add_argument("--configs", default="2")
     ap.add_argument("--scale", type=int, default=1)
     ap.add_argument("--out", default=None)
-    ap.add_argument("--smoother-max-mean-row", type=float, default=300.0,
+    ap.add_argument("--smoother-max-mean-row", type=float, default=0.0,
                     help="GPU smoother level policy (0 = every level on the GPU)")
     a = ap.parse_args()
     res = []
