@@ -55,6 +55,11 @@ struct AfsaiArgs {
     int mcap = 1, hcap = 1024;   // mcap: bound of the final pattern size
     int l_global = 0;            // factor in global scratch (rows too long for shared memory)
     double* lscratch = nullptr;  // [gridDim.x * W][packed(mcap)] when l_global
+    int h_global = 0;            // gradient values in global scratch (large tables)
+    double* hvscratch = nullptr; // [gridDim.x * W][hcap] when h_global
+    int* gscratch = nullptr;     // per warp: column hash (keys, slots), slot keys, slot maps
+    long long gstride = 0;       // ints per warp in gscratch
+    int smap_cap = 0;            // slot-map entries per pattern row (max entries j < i of a row)
     const long long* rows = nullptr;  // rows to process (null: all)
     long long nrows = 0;
     // outputs: pass p of row i
@@ -65,6 +70,7 @@ struct AfsaiArgs {
     const int* ycap = nullptr;
     int* pout = nullptr;         // final pattern, insertion order: pout + i * mcap
     unsigned long long* bad = nullptr;  // smallest failing row
+    unsigned long long* prof = nullptr; // optional: cycles per phase (ASPAMG_AFSAI_PROF)
 };
 
 __host__ __device__ inline size_t packed(long long m) { return (size_t)m * (size_t)(m + 1) / 2; }
@@ -76,16 +82,28 @@ __host__ __device__ inline int pat_cap(int mcap) {
     return c;
 }
 
-__host__ __device__ inline size_t warp_bytes(int mcap, int hcap, bool l_global) {
+__host__ __device__ inline size_t warp_bytes(int mcap, int hcap, bool l_global, bool h_global) {
     const size_t lp = l_global ? 0 : packed(mcap);
-    size_t b = 8 * (lp + 2 * (size_t)mcap + (size_t)hcap) +
-               4 * ((size_t)hcap + (size_t)mcap + 40 + 2 * (size_t)pat_cap(mcap));
+    const size_t hc = h_global ? 0 : (size_t)hcap / 2;  // slot values (the column hash stays <= half full)
+    size_t b = 8 * (lp + 2 * (size_t)mcap + hc) + 4 * (2 * (size_t)mcap + 41 + 40 + 2 * (size_t)pat_cap(mcap) + 4);
     return (b + 15) & ~(size_t)15;
+}
+// per-warp global ints: column hash keys + slots (2 hcap), slot keys (hcap), slot
+// maps of the pattern rows and row i ((mcap + 1) smap_cap)
+__host__ __device__ inline long long gscratch_ints(int mcap, int hcap, int smap_cap) {
+    return 3LL * hcap + (long long)(mcap + 1) * smap_cap;
 }
 
 struct WarpMem {
-    double *L, *y, *a, *hv;
-    int *hk, *pat, *sel, *pk, *pv;
+    double *L, *y, *a;
+    double* sv;      // gradient value per slot
+    int* hk;         // column hash: keys (-1 empty)
+    int* hs;         // column hash: slot of the key
+    int* sk;         // slot -> column (>= 0), or -1 - column once the column is in the pattern
+    int* smap;       // slot maps: pattern position q (mcap: row i) -> slots of row's entries j < i
+    int* slen;       // entries j < i of the row at position q (mcap: row i)
+    int* ns;         // [0] slot count, [1] overflow flag
+    int *pat, *sel, *pk, *pv;
     int pcap;
 };
 
@@ -113,12 +131,28 @@ __device__ __forceinline__ double dot_w32(const double* x, const double* y, int 
     return s;
 }
 
-// smalldense.cpp trsv_lower (left-looking) on the packed factor (b may be the factor's row n).
+// smalldense.cpp trsv_lower on the packed factor (b may be the factor's row n):
+// 32-row blocks, lane l on row B + l — the panel product t = L_i[0..B) . b[0..B)
+// as one sequential chain, then right-looking inside the block (lane j divides,
+// broadcasts, lanes > j update).
 __device__ void trsv_lower_w(int n, const double* L, double* b, int lane) {
-    for (int i = 0; i < n; ++i) {
-        const double* Li = L + packed(i);
-        const double d = dot_w32(Li, b, i, lane);
-        if (lane == 0) b[i] = __ddiv_rn(__dsub_rn(b[i], d), Li[i]);
+    for (int B = 0; B < n; B += 32) {
+        const int i = B + lane;
+        const double* Li = L + packed(i < n ? i : 0);
+        double t = 0.0;
+        if (i < n) {
+#pragma unroll 8
+            for (int k = 0; k < B; ++k) t = __dadd_rn(t, __dmul_rn(Li[k], b[k]));
+        }
+        double bi = i < n ? __dsub_rn(b[i], t) : 0.0;
+        const int nb = min(32, n - B);
+        for (int j = 0; j < nb; ++j) {
+            if (lane == j) bi = __ddiv_rn(bi, Li[i]);
+            const double xj = __shfl_sync(FULL, bi, j);
+            if (lane > j && i < n) bi = __dsub_rn(bi, __dmul_rn(Li[B + j], xj));
+        }
+        __syncwarp();
+        if (i < n) b[i] = bi;
         __syncwarp();
     }
 }
@@ -196,18 +230,33 @@ __device__ bool chol_append_w(const DCsr64& A, const WarpMem& w, int m, long lon
     return true;
 }
 
-__device__ int h_insert(int* hk, double* hv, int hcap, int key, bool& ovf) {
-    unsigned h = hslot(key, hcap);
+// Gradient support (fsai.cpp run_row step (d)). The columns j < i touched by the
+// rows of P + {i} get dense slots once, when a row enters (a column hash maps j
+// to its slot); each row keeps the slot of each of its entries (its slot map).
+// A gradient step then zeroes the slot values and, row by row in the host's
+// order (pattern in insertion order, then i), adds A(r, j) * gm into the
+// entries' slots: the same sum per column as the host's accumulator, with no
+// probing per step. Slot numbering is not deterministic and does not need to
+// be: the candidate choice is a strict total order on (|g|, column).
+__device__ int slot_of(const WarpMem& w, int hcap, int col, bool& ovf) {  // find or create
+    unsigned h = hslot(col, hcap);
     for (int p = 0; p < hcap; ++p) {
-        const int k = hk[h];
-        if (k == key) return (int)h;
+        const int k = w.hk[h];
+        if (k == col) return w.hs[h];  // (a row's columns are distinct: never concurrently created)
         if (k == -1) {
-            const int old = atomicCAS(&hk[h], -1, key);
+            const int old = atomicCAS(&w.hk[h], -1, col);
             if (old == -1) {
-                hv[h] = 0.0;  // first touch: grad[j] = 0.0
-                return (int)h;
+                const int sl = atomicAdd(&w.ns[0], 1);
+                if (sl >= hcap / 2) {  // keep the table at most half full
+                    ovf = true;
+                    w.hs[h] = 0;
+                    return -1;
+                }
+                w.sk[sl] = col;
+                w.hs[h] = sl;
+                return sl;
             }
-            if (old == key) return (int)h;
+            if (old == col) return w.hs[h];
         }
         h = (h + 1) & (unsigned)(hcap - 1);
     }
@@ -215,30 +264,49 @@ __device__ int h_insert(int* hk, double* hv, int hcap, int key, bool& ovf) {
     return -1;
 }
 
-__device__ int h_find(const int* hk, int hcap, int key) {
-    unsigned h = hslot(key, hcap);
+__device__ int slot_find(const WarpMem& w, int hcap, int col) {
+    unsigned h = hslot(col, hcap);
     for (int p = 0; p < hcap; ++p) {
-        const int k = hk[h];
-        if (k == key) return (int)h;
+        const int k = w.hk[h];
+        if (k == col) return w.hs[h];
         if (k == -1) return -1;
         h = (h + 1) & (unsigned)(hcap - 1);
     }
     return -1;
 }
 
-// grad[j] += A(r, j) * gm for the j < i of row r (lanes take distinct j; the
-// row's columns ascend, so the entries past the first j >= i are skipped).
-__device__ void scatter_w(const DCsr64& A, long long r, double gm, long long i, const WarpMem& w, int hcap, int lane,
-                          bool& ovf) {
+// Row r enters the gradient support at pattern position q (mcap: row i): slots for
+// its entries j < i (new slots of columns already in P are marked at once).
+__device__ void support_add(const AfsaiArgs& P, const WarpMem& w, long long r, int q, long long i, int lane,
+                            bool& ovf) {
+    const DCsr64& A = P.A;
     const long long b = A.rp[r], e = A.rp[r + 1];
+    int* sm = w.smap + (long long)q * P.smap_cap;
+    int len = (int)(e - b);  // all entries < i unless a column >= i is met
     for (long long q0 = b; q0 < e; q0 += 32) {
-        const long long q = q0 + lane;
-        const long long j = q < e ? A.ci[q] : LLONG_MAX;
+        const long long t = q0 + lane;
+        const long long j = t < e ? A.ci[t] : LLONG_MAX;
         if (j < i) {
-            const int slot = h_insert(w.hk, w.hv, hcap, (int)j, ovf);
-            if (slot >= 0) w.hv[slot] = __dadd_rn(w.hv[slot], __dmul_rn(A.v[q], gm));
+            const int sl = slot_of(w, P.hcap, (int)j, ovf);
+            sm[t - b] = sl;
+            if (sl >= 0 && pat_find(w, j) >= 0) w.sk[sl] = -1 - (int)j;
         }
-        if (__any_sync(FULL, j >= i)) break;
+        const unsigned ge = __ballot_sync(FULL, j >= i);
+        if (ge) {
+            len = (int)(q0 - b) + __ffs(ge) - 1;
+            break;
+        }
+    }
+    if (lane == 0) w.slen[q] = len;
+    __syncwarp();
+}
+
+// grad[slot(j)] += A(r, j) * gm over row r's entries j < i (lanes take distinct j).
+__device__ void grad_row(const DCsr64& A, const WarpMem& w, long long r, const int* sm, int len, double gm, int lane) {
+    const double* av = A.v + A.rp[r];
+    for (int t = lane; t < len; t += 32) {
+        const int sl = sm[t];
+        w.sv[sl] = __dadd_rn(w.sv[sl], __dmul_rn(av[t], gm));
     }
     __syncwarp();
 }
@@ -248,7 +316,26 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
     const DCsr64& A = P.A;
     const long long n = A.n_rows;
     int m = 0;
+    long long tph = clock64();
+    auto mark = [&](int ph) {
+        if (P.prof) {
+            const long long t = clock64();
+            if (lane == 0) atomicAdd(P.prof + ph, (unsigned long long)(t - tph));
+            tph = t;
+        }
+    };
+    auto fail = [&](int code) {
+        if (lane == 0) {
+            P.cnt[i] = code;
+            if (code == -1) atomicMin(P.bad, (unsigned long long)i);
+        }
+    };
     for (int q = lane; q < w.pcap; q += 32) w.pk[q] = -1;
+    for (int q = lane; q < P.hcap; q += 32) {
+        w.hk[q] = -1;
+        w.hs[q] = -1;
+    }
+    if (lane == 0) w.ns[0] = 0;
     __syncwarp();
     if (P.gs_rp) {
         const long long b = P.gs_rp[i], e = P.gs_rp[i + 1];
@@ -263,16 +350,15 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
         for (int q = 0; q < ns; ++q) {
             if (lane == 0) pat_insert(w, w.pat[q], q);
             __syncwarp();
-            if (!chol_append_w(A, w, m, w.pat[q], lane)) {
-                if (lane == 0) {
-                    P.cnt[i] = -1;
-                    atomicMin(P.bad, (unsigned long long)i);
-                }
-                return;
-            }
+            if (!chol_append_w(A, w, m, w.pat[q], lane)) return fail(-1);
             ++m;
         }
     }
+    bool ovf = false;
+    for (int q = 0; q < m; ++q) support_add(P, w, w.pat[q], q, i, lane, ovf);
+    support_add(P, w, i, P.mcap, i, lane, ovf);
+    if (__any_sync(FULL, ovf)) return fail(-2);
+    mark(0);
     double aii = lane == 0 ? a_at(A, i, i) : 0.0;
     aii = __shfl_sync(FULL, aii, 0);
     double psi = 0.0;
@@ -287,49 +373,39 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
                 gather_row(A, i, i, w, m, w.a, lane);
                 for (int q = lane; q < m; q += 32) w.y[q] = w.a[q];
                 __syncwarp();
+                mark(1);
                 trsv_lower_w(m, w.L, w.y, lane);
+                mark(2);
                 trsv_lower_t_w(m, w.L, w.y, lane);
+                mark(3);
                 psi = __dsub_rn(aii, dot_w32(w.a, w.y, m, lane));
-                if (!(psi > 0.0)) {
-                    if (lane == 0) {
-                        P.cnt[i] = -1;
-                        atomicMin(P.bad, (unsigned long long)i);
-                    }
-                    return;
-                }
+                if (!(psi > 0.0)) return fail(-1);
                 have = true;
             }
             if (step > 0 && __dsub_rn(psi_prev, psi) <= __dmul_rn(eps, psi_prev)) break;
             if (step == k) break;
             psi_prev = psi;
-            // gradient over the rows of P (insertion order) then row i
-            bool ovf = false;
-            for (int s = lane; s < P.hcap; s += 32) w.hk[s] = -1;
+            // gradient: rows of P (insertion order) then row i, into the support's slots
+            const int T = w.ns[0];
+            for (int t = lane; t < T; t += 32) w.sv[t] = 0.0;
             __syncwarp();
-            for (int q = 0; q < m; ++q) scatter_w(A, w.pat[q], -w.y[q], i, w, P.hcap, lane, ovf);
-            scatter_w(A, i, 1.0, i, w, P.hcap, lane, ovf);
-            if (__any_sync(FULL, ovf)) {
-                if (lane == 0) P.cnt[i] = -2;
-                return;
-            }
-            for (int q = lane; q < m; q += 32) {  // exclude the pattern
-                const int sl = h_find(w.hk, P.hcap, w.pat[q]);
-                if (sl >= 0) w.hk[sl] = -2;
-            }
-            __syncwarp();
+            for (int q = 0; q < m; ++q)
+                grad_row(A, w, w.pat[q], w.smap + (long long)q * P.smap_cap, w.slen[q], -w.y[q], lane);
+            grad_row(A, w, i, w.smap + (long long)P.mcap * P.smap_cap, w.slen[P.mcap], 1.0, lane);
+            mark(4);
             // the rho best candidates: |g| descending, then column ascending
             int take = 0;
             for (; take < rho; ++take) {
                 double bv = -1.0;
                 int bj = INT_MAX, bs = -1;
-                for (int s = lane; s < P.hcap; s += 32) {
-                    const int key = w.hk[s];
+                for (int t = lane; t < T; t += 32) {
+                    const int key = w.sk[t];
                     if (key >= 0) {
-                        const double av = fabs(w.hv[s]);
+                        const double av = fabs(w.sv[t]);
                         if (av > bv || (av == bv && key < bj)) {
                             bv = av;
                             bj = key;
-                            bs = s;
+                            bs = t;
                         }
                     }
                 }
@@ -347,10 +423,11 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
                 if (bs < 0) break;
                 if (lane == 0) {
                     w.sel[take] = bj;
-                    w.hk[bs] = -2;
+                    w.sk[bs] = -1 - bj;  // enters the pattern
                 }
                 __syncwarp();
             }
+            mark(5);
             if (take == 0) break;
             if (lane == 0)  // ascending column order of the chosen candidates
                 for (int a = 1; a < take; ++a) {
@@ -370,16 +447,13 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
                     pat_insert(w, j, m);
                 }
                 __syncwarp();
-                if (!chol_append_w(A, w, m, j, lane)) {
-                    if (lane == 0) {
-                        P.cnt[i] = -1;
-                        atomicMin(P.bad, (unsigned long long)i);
-                    }
-                    return;
-                }
+                if (!chol_append_w(A, w, m, j, lane)) return fail(-1);
+                support_add(P, w, j, m, i, lane, ovf);
                 ++m;
             }
+            if (__any_sync(FULL, ovf)) return fail(-2);
             have = false;
+            mark(6);
         }
         double* yo = P.yout + P.yoff[pass] + i * (long long)P.ycap[pass];
         for (int q = lane; q < m; q += 32) yo[q] = w.y[q];
@@ -395,19 +469,32 @@ __device__ void afsai_row(const AfsaiArgs& P, const WarpMem& w, long long i, int
 __global__ void k_afsai(const AfsaiArgs P) {
     extern __shared__ __align__(16) unsigned char dyn[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
-    unsigned char* p = dyn + (size_t)wid * warp_bytes(P.mcap, P.hcap, P.l_global != 0);
+    unsigned char* p = dyn + (size_t)wid * warp_bytes(P.mcap, P.hcap, P.l_global != 0, P.h_global != 0);
+    const size_t gw = (size_t)blockIdx.x * W + wid;
     WarpMem w;
     if (P.l_global) {
-        w.L = P.lscratch + ((size_t)blockIdx.x * W + wid) * packed(P.mcap);
+        w.L = P.lscratch + gw * packed(P.mcap);
     } else {
         w.L = reinterpret_cast<double*>(p);
         p += 8 * packed(P.mcap);
     }
     w.y = reinterpret_cast<double*>(p);
     w.a = w.y + P.mcap;
-    w.hv = w.a + P.mcap;
-    w.hk = reinterpret_cast<int*>(w.hv + P.hcap);
-    w.pat = w.hk + P.hcap;
+    double* after = w.a + P.mcap;
+    if (P.h_global) {
+        w.sv = P.hvscratch + gw * (P.hcap / 2);
+    } else {
+        w.sv = after;
+        after += P.hcap / 2;
+    }
+    w.ns = reinterpret_cast<int*>(after);
+    w.slen = w.ns + 4;
+    w.pat = w.slen + P.mcap + 1;
+    int* g = P.gscratch + gw * P.gstride;
+    w.hk = g;
+    w.hs = g + P.hcap;
+    w.sk = g + 2LL * P.hcap;
+    w.smap = g + 3LL * P.hcap;
     w.sel = w.pat + P.mcap;
     w.pcap = pat_cap(P.mcap);
     w.pk = w.sel + 40;
@@ -575,7 +662,7 @@ double batch_bytes(long long n, long long gs_max, int npass, const PassParams& p
 }
 
 Batch run_passes_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, const DevG* Gs, int npass,
-                        const PassParams& p0, const PassParams& pr) {
+                        const PassParams& p0, const PassParams& pr, int* hcap_hint = nullptr) {
     cudaStream_t s = c->stream;
     const long long n = A.n_rows;
     const long long gs_max = max_row(Gs);  // includes the diagonal: a bound of the start pattern
@@ -611,7 +698,8 @@ Batch run_passes_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, 
     // table sizes: an upper bound of the touched columns, capped; overflowing rows rerun wider
     const long long touch = (long long)(mcap + 1) * std::max<long long>(a_maxrow, 1);
     int hcap = 64;
-    while (hcap < touch && hcap < 2048) hcap <<= 1;
+    while (hcap < 2 * touch && hcap < 4096) hcap <<= 1;
+    if (hcap_hint && *hcap_hint > hcap) hcap = *hcap_hint;  // an earlier batch of this level overflowed
     for (int attempt = 0; attempt < 4; ++attempt) {
         AfsaiArgs P;
         P.A = A;
@@ -640,18 +728,14 @@ Batch run_passes_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, 
             P.rows = drows;
             P.nrows = (long long)todo.size();
         }
-        // rows in flight: the factor in shared memory while it fits, else in a global
-        // scratch sized to stay L2-resident (a few warps per SM)
+        // rows in flight: short factors in shared memory, longer ones in a global
+        // scratch (latency hidden by more warps per SM; the factor sweeps are streams)
         const size_t budget = 200 * 1024;
-        const bool lg = warp_bytes(mcap, hcap, false) > budget;
-        const size_t wb = warp_bytes(mcap, hcap, lg);
+        const bool lg = 8 * packed(mcap) > 24 * 1024;
+        const bool hg = hcap > 4096;
+        const size_t wb = warp_bytes(mcap, hcap, lg, hg);
         if (wb > budget) throw Fail{4, "afsai (GPU): row workspace exceeds shared memory"};
-        int W = (int)std::max<size_t>(1, std::min<size_t>(16, budget / wb));
-        if (lg) {
-            const double per_warp = 8.0 * double(packed(mcap));
-            const int w_l2 = (int)std::max(1.0, 96e6 / (per_warp * sms));  // factors of all warps ~ 96 MB
-            W = std::max(1, std::min(W, w_l2));
-        }
+        const int W = (int)std::max<size_t>(1, std::min<size_t>(16, budget / wb));
         const size_t smem = wb * W;
         CK(cudaFuncSetAttribute(k_afsai, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 1;
@@ -664,9 +748,31 @@ Batch run_passes_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, 
             P.lscratch = dalloc<double>(c, (size_t)grid * W * packed(mcap));
             scratch.push_back(P.lscratch);
         }
+        P.h_global = hg ? 1 : 0;
+        if (hg) {
+            P.hvscratch = dalloc<double>(c, (size_t)grid * W * (hcap / 2));
+            scratch.push_back(P.hvscratch);
+        }
+        P.smap_cap = (int)std::max<long long>(a_maxrow, 1);
+        P.gstride = gscratch_ints(mcap, hcap, P.smap_cap);
+        P.gscratch = dalloc<int>(c, (size_t)grid * W * (size_t)P.gstride);
+        scratch.push_back(P.gscratch);
+        static const bool prof = std::getenv("ASPAMG_AFSAI_PROF") != nullptr;
+        if (prof) {
+            P.prof = dalloc<unsigned long long>(c, 8);
+            scratch.push_back(P.prof);
+            CK(cudaMemsetAsync(P.prof, 0, 64, s));
+        }
         if (rows > 0) {
             k_afsai<<<grid, 32 * W, smem, s>>>(P);
             CK(cudaGetLastError());
+        }
+        if (prof) {
+            unsigned long long h[8];
+            CK(cudaMemcpyAsync(h, P.prof, 64, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::fprintf(stderr, "[afsai prof n=%lld npass=%d mcap=%d hcap=%d W=%d grid=%d lg=%d hg=%d] Gcyc: start %.2f gather %.2f fwd %.2f bwd %.2f grad %.2f cand %.2f append %.2f\n",
+                         rows, npass, mcap, hcap, W, grid, (int)lg, (int)hg, h[0] / 1e9, h[1] / 1e9, h[2] / 1e9, h[3] / 1e9, h[4] / 1e9, h[5] / 1e9, h[6] / 1e9);
         }
         CK(cudaMemcpyAsync(hc.data(), B.cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -674,9 +780,10 @@ Batch run_passes_device(aspamg_gpu_ctx* c, const DCsr64& A, long long a_maxrow, 
         for (long long i = 0; i < n; ++i)
             if (hc[(size_t)i] == -2) todo.push_back(i);
         if (todo.empty()) break;
-        hcap = attempt == 0 ? 4096 : attempt == 1 ? 8192 : 16384;
+        if (hcap_hint && (double)todo.size() > 0.01 * (double)n) *hcap_hint = hcap * 4;  // next batches start wider
+        hcap *= 4;
     }
-    if (!todo.empty()) throw Fail{4, "afsai (GPU): gradient support exceeds 16384 columns in a row"};
+    if (!todo.empty()) throw Fail{4, "afsai (GPU): gradient support exceeds the gradient table in a row"};
     unsigned long long hbad = 0;
     CK(cudaMemcpy(&hbad, bad, 8, cudaMemcpyDeviceToHost));
     for (void* q : scratch) dfree(c, q);
@@ -869,7 +976,7 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
         };
         const PassParams p0{(int)prm->k0, (int)prm->rho0, prm->eps0}, pr{(int)prm->ki, (int)prm->rhoi, prm->epsi};
         Batch B;
-        int next = 0, last_batch = 1;
+        int next = 0, last_batch = 1, hcap_hint = 0;
         std::vector<double> lam_hist, nnzr_hist;
         const bool trace = std::getenv("ASPAMG_SETUP_TRACE") != nullptr;
         DevG G;
@@ -902,7 +1009,7 @@ extern "C" int aspamg_gpu_smoother_setup(void* device, const aspamg_csr_view* A,
                 }
                 last_batch = want;
                 const double t0 = now_s();
-                B = run_passes_device(c, dA.view, a_maxrow, first ? nullptr : &G, want, first ? p0 : pr, pr);
+                B = run_passes_device(c, dA.view, a_maxrow, first ? nullptr : &G, want, first ? p0 : pr, pr, &hcap_hint);
                 next = 0;
                 if (trace)
                     std::fprintf(stderr, "[gpu smoother n=%lld] batch of %d passes: %.2f s\n", n, want, now_s() - t0);

@@ -40,9 +40,25 @@ double dot_w32(const double* a, const double* b, int n) {
     return s[0];
 }
 
-// Left-looking: b_i = (b_i - dot_w32(L_i, b, i)) / L_ii.
+// Blocked in 32-row blocks, the order of a warp with lane l on row B + l:
+// t_i = L_i[0..B) . b[0..B) as one sequential chain, b_i -= t_i; then inside the
+// block, right-looking: b_j /= L_jj, b_i -= L_ij b_j for the block's rows i > j.
 void trsv_lower(int n, const double* L, int ld, double* b) {
-    for (int i = 0; i < n; ++i) b[i] = (b[i] - dot_w32(L + (size_t)i * ld, b, i)) / L[(size_t)i * ld + i];
+    for (int B = 0; B < n; B += 32) {
+        const int nb = std::min(32, n - B);
+        double bi[32];
+        for (int l = 0; l < nb; ++l) {
+            const double* Li = L + (size_t)(B + l) * ld;
+            double t = 0.0;
+            for (int k = 0; k < B; ++k) t += Li[k] * b[k];
+            bi[l] = b[B + l] - t;
+        }
+        for (int j = 0; j < nb; ++j) {
+            bi[j] = bi[j] / L[(size_t)(B + j) * ld + B + j];
+            for (int l = j + 1; l < nb; ++l) bi[l] = bi[l] - L[(size_t)(B + l) * ld + B + j] * bi[j];
+        }
+        for (int l = 0; l < nb; ++l) b[B + l] = bi[l];
+    }
 }
 
 // Right-looking: b_i /= L_ii, then b_k -= L_ik b_i for k < i (i descending).

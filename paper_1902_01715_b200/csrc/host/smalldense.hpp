@@ -14,8 +14,8 @@ long cholesky_lower(int n, double* a);
 // sum_k a[k] b[k] in the order of a 32-lane warp reduction: 32 strided partial
 // sums combined by the xor butterfly (deterministic; the device aFSAI's order).
 double dot_w32(const double* a, const double* b, int n);
-// Solve L y = b in place (L row-major lower, leading dimension ld), left-looking
-// with dot_w32 row products.
+// Solve L y = b in place (L row-major lower, leading dimension ld), in 32-row
+// blocks: sequential panel products, right-looking inside the block (a warp's order).
 void trsv_lower(int n, const double* L, int ld, double* b);
 // Solve L' y = b in place, right-looking (b_k -= L_ik b_i, i descending).
 void trsv_lower_t(int n, const double* L, int ld, double* b);
