@@ -103,24 +103,6 @@ void slice_meta(const std::vector<int>& len, std::vector<int2>& meta, long long&
     }
 }
 
-// True when the columns of every block of 32 consecutive rows fit in
-// [min, min + 65535] (row-segment layout: one base per block).
-bool blocks_fit_u16(const aspamg_csr_view& v) {
-    const int64_t nq = (v.n_rows + 31) / 32;
-    int ok = 1;
-#pragma omp parallel for schedule(static) reduction(&& : ok)
-    for (int64_t q = 0; q < nq; ++q) {
-        const int64_t b = v.row_offsets[32 * q], e = v.row_offsets[std::min<int64_t>(32 * q + 32, v.n_rows)];
-        int64_t lo = INT64_MAX, hi = -1;
-        for (int64_t k = b; k < e; ++k) {
-            lo = std::min(lo, v.col_indices[k]);
-            hi = std::max(hi, v.col_indices[k]);
-        }
-        if (e > b && hi - lo > 65535) ok = 0;
-    }
-    return ok != 0;
-}
-
 // True when every row's columns fit in [first, first + 65535] (sorted rows).
 bool rows_fit_u16(const aspamg_csr_view& v) {
     int ok = 1;
@@ -182,9 +164,6 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     }
     bool sell = v.n_rows >= c->opt_sell_min_rows && mean <= (double)c->opt_sell_max_mean &&
                 mean >= (double)c->opt_sell_min_mean && maxlen <= c->opt_sell_max_len;
-    const bool rseg = c->opt_rseg > 0 && v.n_rows > 0 && v.n_rows >= c->opt_rseg_min_rows &&
-                      mean <= (double)c->opt_rseg_max_mean;
-    if (rseg && c->opt_rseg >= 2) sell = false;
     if (sell && c->opt_sell_chh == 0 && !c->opt_sell_sort && nnz > 0) {
         // natural order only (sorted SELL loses the x-gather locality): fall back
         // to CSR when neither chunk height pads <= the limit
@@ -216,7 +195,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         std::vector<int> perm;
         std::vector<int> slen = len;
         int h = 32;
-        if (c->opt_sell_chh == 8 || (c->opt_sell_chh == 0 && !c->opt_sell_tma && f32 > lim && f8 <= lim)) {
+        if (c->opt_sell_chh == 8 || (c->opt_sell_chh == 0 && f32 > lim && f8 <= lim)) {
             h = 8;
             meta.swap(meta8);
             S.slots = s8;
@@ -236,7 +215,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         }
         S.chh = h;
         // S.slots counts slot rows of h entries; store padded entries / 32 for the byte accounting
-        const bool i16 = c->opt_idx16 && !c->opt_sell_tma && rows_fit_u16(v);
+        const bool i16 = c->opt_idx16 && rows_fit_u16(v);
         const size_t nslot = (size_t)std::max<long long>(S.slots * h, 1);
         std::vector<int> ci(i16 ? 0 : nslot, 0), cb(i16 ? (size_t)std::max<int64_t>(v.n_rows, 1) : 0, 0);
         std::vector<unsigned short> c16(i16 ? nslot : 0, 0);
@@ -280,7 +259,6 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
         // U*10 + min CTAs/SM. Large operators: U = 4 at 4 CTAs/SM (64 registers) keeps more
         // warps in flight (C2 level-0 G: 35 vs 40 us); smaller ones keep U = 8 (tools/tune_kernels.py)
         S.u = c->opt_sell_u > 0 ? (int)c->opt_sell_u : (maxlen <= 4 ? 41 : v.n_rows >= 400000 ? 44 : 83);
-        S.tma = (int)c->opt_sell_tma;  // SEG*10 + stages, 0 = register pipeline
         return M;
     }
     M.fmt = 0;
@@ -289,10 +267,8 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     A.n_cols = (int)v.n_cols;
     A.nnz = nnz;
     A.group = group_for(mean, maxlen, v.n_rows, (double)c->opt_csr_per_thread);
-    if (rseg) A.rseg = c->opt_rseg_u > 0 ? (int)c->opt_rseg_u : 84;
-    A.u8 = (int)c->opt_csr_u8;
     A.pf = (int)c->opt_csr_pf;
-    if (c->opt_csr_long > 0 && !rseg && A.group <= 16 && !(c->opt_csr_vec && A.group >= 16)) {
+    if (c->opt_csr_long > 0 && A.group <= 16) {
         const int thr = (int)c->opt_csr_long * A.group * 4;
         std::vector<int> lr;
         for (int64_t i = 0; i < v.n_rows; ++i)
@@ -308,25 +284,12 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     // 16-bit offsets pay off for short rows (few threads per row, index bytes a
     // larger share of the per-thread stream); long-row operands (group >= 32)
     // measured slower with them (tools/tune_kernels.py, profiles/README.md).
-    // Row-segment mode: one base column per 32-row block.
-    const bool vec = c->opt_csr_vec && !rseg && A.group >= 16;
-    const bool i16 = c->opt_idx16 && (rseg ? blocks_fit_u16(v) : (vec || A.group <= c->opt_idx16_max_group) && rows_fit_u16(v));
-    A.vec = vec && i16;
-    const int64_t nbase = rseg ? (v.n_rows + 31) / 32 : v.n_rows;
+    const bool i16 = c->opt_idx16 && A.group <= c->opt_idx16_max_group && rows_fit_u16(v);
+    const int64_t nbase = v.n_rows;
     std::vector<int> rp((size_t)v.n_rows + 1), ci(i16 ? 0 : (size_t)nnz), cb(i16 ? (size_t)std::max<int64_t>(nbase, 1) : 0);
     std::vector<unsigned short> c16(i16 ? (size_t)nnz : 0);
     for (int64_t i = 0; i <= v.n_rows; ++i) rp[(size_t)i] = (int)(v.n_rows ? v.row_offsets[i] : 0);
-    if (i16 && rseg) {
-#pragma omp parallel for schedule(static)
-        for (int64_t q = 0; q < nbase; ++q) {
-            const int64_t b = v.row_offsets[32 * q], e = v.row_offsets[std::min<int64_t>(32 * q + 32, v.n_rows)];
-            int64_t base = INT64_MAX;
-            for (int64_t k = b; k < e; ++k) base = std::min(base, v.col_indices[k]);
-            if (e == b) base = 0;
-            cb[(size_t)q] = (int)base;
-            for (int64_t k = b; k < e; ++k) c16[(size_t)k] = (unsigned short)(v.col_indices[k] - base);
-        }
-    } else if (i16) {
+    if (i16) {
 #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < v.n_rows; ++i) {
             const int64_t b = v.row_offsets[i], e = v.row_offsets[i + 1];
@@ -359,7 +322,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
 double mat_bytes(const DMat& M) {
     if (M.fmt == 1) return 76.0 * 32.0 * double(M.sb.slots) + 4.0 * M.sb.nb;
     if (M.fmt == 2) return (M.sell.ci16 ? 10.0 : 12.0) * 32.0 * double(M.sell.slots) + (M.sell.ci16 ? 8.0 : 4.0) * M.sell.n_rows;
-    const double nb = M.csr.rseg ? double((M.csr.n_rows + 31) / 32) : double(M.csr.n_rows);
+    const double nb = double(M.csr.n_rows);
     return (M.csr.ci16 ? 10.0 : 12.0) * double(M.csr.nnz) + 4.0 * (M.csr.n_rows + 1) + (M.csr.ci16 ? 4.0 * nb : 0.0);
 }
 void set_pol(DMat& M, int pol) {
@@ -384,8 +347,8 @@ double alg_bytes(const DMat& M) {
     }
     const double nnz = double(M.fmt == 2 ? M.sell.nnz : M.csr.nnz);
     const bool i16 = M.fmt == 2 ? M.sell.ci16 != nullptr : M.csr.ci16 != nullptr;
-    // 16-bit offsets: 2 B per entry + a 4-B base column per row (per 32-row block in row-segment mode)
-    const double nb = (M.fmt == 0 && M.csr.rseg) ? double((M.rows() + 31) / 32) : double(M.rows());
+    // 16-bit offsets: 2 B per entry + a 4-B base column per row
+    const double nb = double(M.rows());
     const double idx = i16 ? 2.0 * nnz + 4.0 * nb : 4.0 * nnz;
     return 8.0 * nnz + idx + 4.0 * (M.rows() + 1) + 8.0 * M.cols() + 8.0 * M.rows();
 }
@@ -394,7 +357,6 @@ std::string fmt_name(const DMat& M) {
     const bool h = M.fmt == 2 ? M.sell.ci16 != nullptr : M.fmt == 0 && M.csr.ci16 != nullptr;
     const std::string base = M.fmt == 1   ? "sbsr3"
                              : M.fmt == 2 ? (M.sell.perm ? "sells" : M.sell.chh == 8 ? "sell8" : "sell")
-                             : M.csr.rseg ? (M.csr.rseg >= 1000 ? "rsegp" : "rseg") + std::to_string((M.csr.rseg % 1000) / 10)
                                           : "csr" + std::to_string(M.csr.group);
     return h ? base + "h" : base;  // h: 16-bit column offsets
 }
@@ -413,7 +375,7 @@ void add_spmv(aspamg_gpu_ctx* c, std::vector<Op>& ops, const std::string& name, 
                        Launch L{grid, s};
                        spmv(Mc, epi, x, y, aux, omega, dotw, red, done, L);
                    }});
-    if (M.fmt == 0 && !M.csr.rseg && !M.csr.nlong && fin == FIN_NONE && !dotw) {
+    if (M.fmt == 0 && !M.csr.nlong && fin == FIN_NONE && !dotw) {
         Op& o = ops.back();
         o.describable = true;
         o.desc.kind = 0;
@@ -874,15 +836,9 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "tail_rows") c->opt_tail_rows = value;
         else if (k == "csr_per_thread") c->opt_csr_per_thread = std::max<int64_t>(1, value);
         else if (k == "idx16") c->opt_idx16 = value;
-        else if (k == "rseg") c->opt_rseg = value;
-        else if (k == "csr_u8") c->opt_csr_u8 = value;
         else if (k == "csr_pf") c->opt_csr_pf = value;
         else if (k == "csr_long") c->opt_csr_long = value;
-        else if (k == "csr_vec") c->opt_csr_vec = value;
         else if (k == "tail_dense") c->opt_tail_dense = value;
-        else if (k == "rseg_u") c->opt_rseg_u = value;
-        else if (k == "rseg_max_mean") c->opt_rseg_max_mean = value;
-        else if (k == "rseg_min_rows") c->opt_rseg_min_rows = value;
         else if (k == "idx16_max_group") c->opt_idx16_max_group = value;
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;
         else if (k == "sell_max_len") c->opt_sell_max_len = value;
@@ -890,7 +846,6 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "sell_sigma") c->opt_sell_sigma = value;
         else if (k == "sell_sort_fill_pct") c->opt_sell_sort_fill_pct = value;
         else if (k == "sell_u") c->opt_sell_u = value;
-        else if (k == "sell_tma") c->opt_sell_tma = value;
         else if (k == "sell_chh") c->opt_sell_chh = value;
         else if (k == "sell_sort") c->opt_sell_sort = value;
         else if (k == "sell_min_mean") c->opt_sell_min_mean = value;

@@ -67,18 +67,13 @@ struct aspamg_gpu_ctx {
     // options
     int opt_bsr = 1, opt_device_loop = 1, opt_coarse_mode = 1;
     long long opt_sell_min_rows = 65536, opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
-              opt_sell_u = 0, opt_sell_tma = 0, opt_sell_chh = 0, opt_sell_sort = 0,
+              opt_sell_u = 0, opt_sell_chh = 0, opt_sell_sort = 0,
               opt_sell_min_mean = 8;
-    // row-segment CSR kernel (k_rseg): 0 off, 1 for CSR-format short-row operands,
-    // 2 also instead of SELL; rseg_u = variant (U*10 + CTAs/SM, 0 = auto)
-    long long opt_csr_u8 = 0;  // CSR: 8 loads per thread per round (1: T >= 32, 2: every T)
     // collapse the V-cycle below the first level with <= this many rows (0 = off);
     // C2 0.995 -> 0.966 ms/it, C1 0.120 -> 0.107 ms/it (profiles/tune_r01_tail_long.log)
     long long opt_tail_dense = 1500;
     long long opt_csr_long = 4;  // long-row split threshold in rounds (rows > long*T*4 entries; 0 = off)
-    long long opt_csr_vec = 0;  // 16-bit long-row operands (T >= 16) with the quad-vectorized kernel
     long long opt_csr_pf = 1;  // CSR (T <= 16): prefetch the next row's pointers (measured 1.4% faster per PCG iteration on C2)
-    long long opt_rseg = 0, opt_rseg_u = 0, opt_rseg_max_mean = 64, opt_rseg_min_rows = 65536;
     long long opt_idx16 = 1;  // 16-bit column offsets where every row spans < 2^16 columns
     long long opt_idx16_max_group = 16;  // ... and (CSR) at most this many threads per row
     long long opt_stream_bytes = 48ll << 20, opt_keep_bytes = 64ll << 20, opt_tail_rows = 0, opt_csr_per_thread = 4;

@@ -329,278 +329,6 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
 }
 
-// ------------------------------------------------- vectorized 16-bit CSR SpMV
-// Long-row operands with 16-bit column offsets (10 matrix bytes per entry):
-// each thread takes aligned quads of 4 consecutive entries — two 16-B value
-// loads and one 8-B index load per quad instead of four 8-B + four 2-B loads —
-// QU quads per round; the unaligned head / tail entries of a row are handled
-// one per thread. Per-thread fma chains in quad order, then the same fixed
-// shuffle (+ smem for T > 32) tree as k_csr: deterministic, within the CSR
-// tolerance of the reference order.
-template <class T>
-__device__ __forceinline__ T ld_vec(const T* p, int pol) {
-    return pol == 1 ? __ldcs(p) : __ldg(p);
-}
-template <int T, int STREAM, int QU = 2>
-__global__ void __launch_bounds__(kBlock) k_csrv(DCsr M, int epi, const double* __restrict__ x, double* y,
-                                                  const double* aux, double omega, const double* dotw, Red red,
-                                                  const int* done) {
-    pdl_enter();
-    if (is_done(done)) return;
-    constexpr int RPC = kBlock / T;
-    __shared__ double wsum[kBlock / 32];
-    const int t = threadIdx.x % T;
-    const int lr = threadIdx.x / T;
-    const int lane = threadIdx.x & 31;
-    double dacc = 0.0;
-    for (int rbase = blockIdx.x * RPC; rbase < M.n_rows; rbase += gridDim.x * RPC) {
-        const int row = rbase + lr;
-        double s = 0.0;
-        if (row < M.n_rows) {
-            const int b = __ldg(M.rp + row), e = __ldg(M.rp + row + 1);
-            const double* xr = x + __ldg(M.cb + row);
-            const int b4 = min((b + 3) & ~3, e), e4 = max(e & ~3, b4);
-            // head (< 4 entries) and tail (< 4 entries): one entry per thread
-            if (t < b4 - b) {
-                const int k = b + t;
-                s = fma(ld_mat<STREAM>(M.v + k), __ldg(xr + ld_mat<STREAM>(M.ci16 + k)), s);
-            }
-            for (int q0 = b4 + 4 * t; q0 < e4; q0 += 4 * T * QU) {
-                double2 va[QU], vb[QU];
-                ushort4 c[QU];
-#pragma unroll
-                for (int u = 0; u < QU; ++u) {
-                    const int k = q0 + 4 * T * u;
-                    va[u] = make_double2(0.0, 0.0);
-                    vb[u] = va[u];
-                    c[u] = make_ushort4(0, 0, 0, 0);
-                    if (k < e4) {
-                        va[u] = ld_vec(reinterpret_cast<const double2*>(M.v + k), STREAM);
-                        vb[u] = ld_vec(reinterpret_cast<const double2*>(M.v + k + 2), STREAM);
-                        c[u] = ld_vec(reinterpret_cast<const ushort4*>(M.ci16 + k), STREAM);
-                    }
-                }
-                double xv[QU][4];
-#pragma unroll
-                for (int u = 0; u < QU; ++u) {
-                    const bool p = q0 + 4 * T * u < e4;
-                    xv[u][0] = p ? __ldg(xr + c[u].x) : 0.0;
-                    xv[u][1] = p ? __ldg(xr + c[u].y) : 0.0;
-                    xv[u][2] = p ? __ldg(xr + c[u].z) : 0.0;
-                    xv[u][3] = p ? __ldg(xr + c[u].w) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < QU; ++u) {
-                    s = fma(va[u].x, xv[u][0], s);
-                    s = fma(va[u].y, xv[u][1], s);
-                    s = fma(vb[u].x, xv[u][2], s);
-                    s = fma(vb[u].y, xv[u][3], s);
-                }
-            }
-            if (t < e - e4) {
-                const int k = e4 + t;
-                s = fma(ld_mat<STREAM>(M.v + k), __ldg(xr + ld_mat<STREAM>(M.ci16 + k)), s);
-            }
-        }
-        if constexpr (T <= 32) {
-#pragma unroll
-            for (int o = T / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, T);
-        } else {
-            s = warp_sum(s);
-            if (lane == 0) wsum[threadIdx.x >> 5] = s;
-            __syncthreads();
-            if (t == 0) {
-                double a = 0.0;
-#pragma unroll
-                for (int w = 0; w < T / 32; ++w) a += wsum[(threadIdx.x >> 5) + w];
-                s = a;
-            }
-            __syncthreads();
-        }
-        if (t == 0 && row < M.n_rows) {
-            const double out = epilogue(epi, s, aux, row, omega);
-            y[row] = out;
-            if (dotw) dacc = fma(out, dotw[row], dacc);
-        }
-    }
-    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
-}
-
-// ---------------------------------------------------- row-segment CSR SpMV
-// A warp owns 32 consecutive rows (lane l <-> row r0 + l). Their entries form
-// one contiguous CSR segment [rp[r0], rp[r0+32]); the warp streams it in tiles
-// of 32*U entries, lane l loading entries t0 + l + 32u (fully coalesced, no
-// padding, U value + U index loads then U x gathers in flight per lane), and
-// writes the products v*x (separately rounded multiply) to a per-warp shared
-// tile. Each lane then adds the products of its own row in ascending column
-// order — the reference spmv's sequential sum (sparse_matrix.cpp:100-105) with
-// separate multiply/add, so y is bit-identical to it regardless of row length
-// or how the segment splits into tiles.
-template <int U, int STREAM, bool I16, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) k_rseg(DCsr M, int epi, const double* __restrict__ x, double* y,
-                                                      const double* aux, double omega, const double* dotw, Red red,
-                                                      const int* done) {
-    pdl_enter();
-    if (is_done(done)) return;
-    constexpr int TILE = 32 * U;
-    __shared__ double prod[kBlock / 32][TILE];
-    const int lane = threadIdx.x & 31;
-    double* sp = prod[threadIdx.x >> 5];
-    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * kBlock) >> 5;
-    const int n = M.n_rows;
-    const int nblk = (n + 31) >> 5;
-    double dacc = 0.0;
-    for (int blk = warp; blk < nblk; blk += nwarps) {
-        const int row = blk * 32 + lane;
-        const bool act = row < n;
-        const int b = __ldg(M.rp + min(row, n));
-        int e = __shfl_down_sync(0xffffffffu, b, 1);
-        if (lane == 31) e = __ldg(M.rp + min(row + 1, n));
-        if (!act) e = b;
-        const int s0 = __shfl_sync(0xffffffffu, b, 0);
-        const int s1 = __shfl_sync(0xffffffffu, e, 31);
-        const double* xb = I16 ? x + __ldg(M.cb + blk) : x;
-        double s = 0.0;
-        int k = b;
-        for (int t0 = s0; t0 < s1; t0 += TILE) {
-            const int t1 = min(t0 + TILE, s1);
-            double v[U], xv[U];
-            int c[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int kk = t0 + lane + 32 * u;
-                v[u] = 0.0;
-                c[u] = 0;
-                if (kk < t1) {
-                    v[u] = ld_mat<STREAM>(M.v + kk);
-                    if constexpr (I16) c[u] = ld_mat<STREAM>(M.ci16 + kk);
-                    else c[u] = ld_mat<STREAM>(M.ci + kk);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = (t0 + lane + 32 * u < t1) ? __ldg(xb + c[u]) : 0.0;
-#pragma unroll
-            for (int u = 0; u < U; ++u) sp[lane + 32 * u] = __dmul_rn(v[u], xv[u]);
-            __syncwarp();
-            const int ke = min(e, t1);
-            for (; k < ke; ++k) s = __dadd_rn(s, sp[k - t0]);
-            __syncwarp();
-        }
-        if (act) {
-            const double out = epilogue(epi, s, aux, row, omega);
-            y[row] = out;
-            if (dotw) dacc = fma(out, dotw[row], dacc);
-        }
-    }
-    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
-}
-
-// Pipelined row-segment kernel: same layout, tiles and arithmetic as k_rseg
-// (bit-identical results), but the matrix loads of the NEXT tile (of this
-// block, or the first tile of the warp's next block, whose row pointers are
-// fetched one block ahead) are issued before the current tile's products are
-// formed and summed, so each warp keeps two tiles of loads in flight and the
-// row-pointer / sum latencies hide behind them.
-template <int U, int STREAM, bool I16, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) k_rsegp(DCsr M, int epi, const double* __restrict__ x, double* y,
-                                                       const double* aux, double omega, const double* dotw, Red red,
-                                                       const int* done) {
-    pdl_enter();
-    if (is_done(done)) return;
-    constexpr int TILE = 32 * U;
-    __shared__ double prod[kBlock / 32][TILE];
-    const int lane = threadIdx.x & 31;
-    double* sp = prod[threadIdx.x >> 5];
-    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * kBlock) >> 5;
-    const int n = M.n_rows;
-    const int nblk = (n + 31) >> 5;
-    double dacc = 0.0;
-    // block state: own row extent [b, e), segment [s0, s1), 16-bit base
-    auto block_rows = [&](int blk, int& b, int& e, int& s0, int& s1, int& cb) {
-        const int row = blk * 32 + lane;
-        b = __ldg(M.rp + min(row, n));
-        e = __shfl_down_sync(0xffffffffu, b, 1);
-        if (lane == 31) e = __ldg(M.rp + min(row + 1, n));
-        if (row >= n) e = b;
-        s0 = __shfl_sync(0xffffffffu, b, 0);
-        s1 = __shfl_sync(0xffffffffu, e, 31);
-        cb = I16 ? __ldg(M.cb + blk) : 0;
-    };
-    double v[U];
-    int c[U];
-    auto load_tile = [&](int t0, int t1) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int kk = t0 + lane + 32 * u;
-            v[u] = 0.0;
-            c[u] = 0;
-            if (kk < t1) {
-                v[u] = ld_mat<STREAM>(M.v + kk);
-                if constexpr (I16) c[u] = ld_mat<STREAM>(M.ci16 + kk);
-                else c[u] = ld_mat<STREAM>(M.ci + kk);
-            }
-        }
-    };
-    int blk = warp;
-    if (blk >= nblk) {
-        if (red.fin != FIN_NONE) reduce_finish(dacc, red);
-        return;
-    }
-    int b, e, s0, s1, cb;
-    block_rows(blk, b, e, s0, s1, cb);
-    int t0 = s0;
-    load_tile(t0, min(t0 + TILE, s1));
-    double s = 0.0;
-    int k = b;
-    while (true) {
-        const int t1 = min(t0 + TILE, s1);
-        const bool last_tile = t0 + TILE >= s1;
-        // next tile coordinates (next block's row pointers fetched now)
-        int nb = blk, nb_b = b, nb_e = e, nb_s0 = s0, nb_s1 = s1, nb_cb = cb, nt0 = t0 + TILE;
-        if (last_tile) {
-            nb = blk + nwarps;
-            if (nb < nblk) {
-                block_rows(nb, nb_b, nb_e, nb_s0, nb_s1, nb_cb);
-                nt0 = nb_s0;
-            }
-        }
-        const double* xb = x + cb;
-        double xv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = (t0 + lane + 32 * u < t1) ? __ldg(xb + c[u]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = __dmul_rn(v[u], xv[u]);
-        if (nb < nblk) load_tile(nt0, min(nt0 + TILE, nb_s1));
-#pragma unroll
-        for (int u = 0; u < U; ++u) sp[lane + 32 * u] = xv[u];
-        __syncwarp();
-        const int ke = min(e, t1);
-        for (; k < ke; ++k) s = __dadd_rn(s, sp[k - t0]);
-        __syncwarp();
-        if (last_tile) {
-            const int row = blk * 32 + lane;
-            if (row < n) {
-                const double out = epilogue(epi, s, aux, row, omega);
-                y[row] = out;
-                if (dotw) dacc = fma(out, dotw[row], dacc);
-            }
-            if (nb >= nblk) break;
-            blk = nb;
-            b = nb_b;
-            e = nb_e;
-            s0 = nb_s0;
-            s1 = nb_s1;
-            cb = nb_cb;
-            s = 0.0;
-            k = b;
-        }
-        t0 = nt0;
-    }
-    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
-}
-
 constexpr int SB_U = 3;    // block slots per load group (sliced BSR3)
 
 // ------------------------------------------------------- sliced BSR3 SpMV
@@ -812,179 +540,6 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const d
             if (dotw) dacc = fma(out, cu.dw, dacc);
         }
         ch = chn;
-    }
-    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
-}
-
-// ------------------------------------------------- SELL-32 SpMV, TMA-staged
-// Same SELL-32 layout and arithmetic as k_sell, but the matrix stream (values +
-// column indices of each chunk segment, two contiguous runs) is moved into a
-// per-warp shared-memory ring by cp.async.bulk (TMA bulk copies) completing on
-// mbarriers. Lane 0 keeps S segments in flight ahead of the consumer, so the
-// bytes in flight per SM are bounded by shared memory, not registers; the lanes
-// only issue the x gathers (addresses read from shared memory) and the sums.
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
-    unsigned ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    while (!mbar_try_wait(bar, parity)) {
-    }
-}
-template <bool EVICT_FIRST>
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-    if constexpr (EVICT_FIRST) {
-        unsigned long long pol;
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-                smem_u32(dst)),
-            "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-            : "memory");
-    } else {
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(dst)),
-                     "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                     : "memory");
-    }
-}
-// Read-only gather whose issue order is pinned (volatile asm is not reordered
-// against other volatile asm): used to force a batch of independent gathers
-// to be in flight together before the dependent arithmetic.
-__device__ __forceinline__ double ldg_pinned(const double* p) {
-    double r;
-    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
-    return r;
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-template <int SEG, int S>
-struct SellTmaCfg {
-    static constexpr int kStageBytes = SEG * 384;                 // SEG slots x (32 doubles + 32 ints)
-    static constexpr int kWarpBytes = 128 + S * kStageBytes;       // barriers padded to 128 B
-    static constexpr int kBlockBytes = (kBlock / 32) * kWarpBytes;
-    static constexpr int kMinBlocks = (220 * 1024) / kBlockBytes < 1 ? 1 : ((220 * 1024) / kBlockBytes > 8 ? 8 : (220 * 1024) / kBlockBytes);
-};
-
-template <int SEG, int S, bool STREAM>
-__global__ void __launch_bounds__(kBlock, (SellTmaCfg<SEG, S>::kMinBlocks)) k_sell_tma(DSell M, int epi, const double* __restrict__ x, double* y,
-                                                      const double* aux, double omega, const double* dotw, Red red,
-                                                      const int* done) {
-    pdl_enter();
-    if (is_done(done)) return;
-    using Cfg = SellTmaCfg<SEG, S>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * kBlock) >> 5;
-    unsigned char* wbase = smem_raw + wib * Cfg::kWarpBytes;
-    unsigned long long* bars = reinterpret_cast<unsigned long long*>(wbase);
-    auto stage_v = [&](int st) { return reinterpret_cast<double*>(wbase + 128 + st * Cfg::kStageBytes); };
-    auto stage_c = [&](int st) { return reinterpret_cast<int*>(wbase + 128 + st * Cfg::kStageBytes + SEG * 256); };
-    if (lane == 0) {
-#pragma unroll
-        for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    const bool need_aux = epi == EPI_RESID || epi == EPI_ADD || epi == EPI_ADDSCALE;
-
-    // producer cursor (uniform across the warp; lane 0 issues)
-    int pch = warp, pseg = 0, pw = 0, poff = 0;
-    if (pch < M.nchunks) {
-        const int2 m = __ldg(M.meta + pch);
-        poff = m.x;
-        pw = m.y;
-    }
-    auto issue = [&](int st) {
-        const int nsl = max(0, min(SEG, pw - pseg * SEG));
-        if (lane == 0) {
-            mbar_expect_tx(&bars[st], (unsigned)(nsl * 384));
-            if (nsl > 0) {
-                const long long slot = (long long)poff + (long long)pseg * SEG;
-                bulk_g2s<STREAM>(stage_v(st), M.v + slot * 32, (unsigned)(nsl * 256), &bars[st]);
-                bulk_g2s<STREAM>(stage_c(st), M.ci + slot * 32, (unsigned)(nsl * 128), &bars[st]);
-            }
-        }
-        ++pseg;
-        if (pseg * SEG >= max(pw, 1)) {
-            pch += nwarps;
-            pseg = 0;
-            if (pch < M.nchunks) {
-                const int2 m = __ldg(M.meta + pch);
-                poff = m.x;
-                pw = m.y;
-            }
-        }
-    };
-#pragma unroll
-    for (int st = 0; st < S; ++st)
-        if (pch < M.nchunks) issue(st);
-
-    double dacc = 0.0;
-    unsigned parity = 0;  // bit st = phase of stage st
-    int stage = 0;
-    for (int ch = warp; ch < M.nchunks; ch += nwarps) {
-        const int srow = ch * 32 + lane;
-        const bool act = srow < M.n_rows;
-        const int len = act ? __ldg(M.len + srow) : 0;
-        const int row = act ? (M.perm ? __ldg(M.perm + srow) : srow) : 0;
-        const double av = (act && need_aux) ? aux[row] : 0.0;
-        const double dw = (act && dotw) ? dotw[row] : 0.0;
-        const int w = __ldg(M.meta + ch).y;
-        const int nseg = max(1, (w + SEG - 1) / SEG);
-        double s = 0.0;
-        for (int sg = 0; sg < nseg; ++sg) {
-            mbar_wait(&bars[stage], (parity >> stage) & 1u);
-            parity ^= 1u << stage;
-            const double* sv = stage_v(stage);
-            const int* sc = stage_c(stage);
-            const int j0 = sg * SEG;
-            // all SEG gathers issued before the first use (padding reads x[0], never used)
-            int ci[SEG];
-            double xv[SEG];
-#pragma unroll
-            for (int j = 0; j < SEG; ++j) ci[j] = (j0 + j < len) ? sc[j * 32 + lane] : 0;
-#pragma unroll
-            for (int j = 0; j < SEG; ++j) xv[j] = ldg_pinned(x + ci[j]);
-#pragma unroll
-            for (int j = 0; j < SEG; ++j)
-                if (j0 + j < len) s = __dadd_rn(s, __dmul_rn(sv[j * 32 + lane], xv[j]));
-            __syncwarp();
-            if (pch < M.nchunks) {
-                if (lane == 0) fence_proxy_async();
-                issue(stage);
-            }
-            stage = stage + 1 == S ? 0 : stage + 1;
-        }
-        if (act) {
-            double out;
-            switch (epi) {
-                case EPI_SCALE: out = __dmul_rn(omega, s); break;
-                case EPI_RESID: out = __dsub_rn(av, s); break;
-                case EPI_ADD: out = __dadd_rn(av, s); break;
-                case EPI_ADDSCALE: out = __dadd_rn(av, __dmul_rn(omega, s)); break;
-                default: out = s;
-            }
-            y[row] = out;
-            if (dotw) dacc = fma(out, dw, dacc);
-        }
     }
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
 }
@@ -1256,51 +811,24 @@ int occ_grid(K kern, long long work_units_per_cta_needed, size_t smem = 0) {
 #define SELLK(UU, P, MB)                                                                            \
     (M.sell.chh == 32 ? (M.sell.ci16 ? k_sell<UU, P, MB, true, 32> : k_sell<UU, P, MB, false, 32>)   \
                       : (M.sell.ci16 ? k_sell<UU, P, MB, true, 0> : k_sell<UU, P, MB, false, 0>))
-// CSR kernel variant of an operand: u8 = 1 eight loads per thread per round for
-// long rows (T >= 32), u8 = 2 for every T; pf = row-pointer prefetch (T <= 16).
+// CSR kernel variant of an operand: pf = row-pointer prefetch (T <= 16).
 using SpmvKern = void (*)(DCsr, int, const double*, double*, const double*, double, const double*, Red, const int*);
 template <int GG, int P, bool I16>
 SpmvKern csr_kernel_i(const DCsr& A) {
-    if constexpr (I16 && GG >= 16) {
-        if (A.vec) return k_csrv<GG, P>;
-    }
-    const bool u8 = A.u8 == 2 || (A.u8 == 1 && GG >= 32);
     if constexpr (GG <= 16) {
-        if (A.pf) return u8 ? k_csr<GG, P, I16, 8, true> : k_csr<GG, P, I16, 4, true>;
+        if (A.pf) return k_csr<GG, P, I16, 4, true>;
     }
-    return u8 ? k_csr<GG, P, I16, 8> : k_csr<GG, P, I16, 4>;
+    return k_csr<GG, P, I16, 4>;
 }
 template <int GG, int P>
 SpmvKern csr_kernel(const DCsr& A) {
     return A.ci16 ? csr_kernel_i<GG, P, true>(A) : csr_kernel_i<GG, P, false>(A);
 }
 #define CSRK(GG, P) csr_kernel<GG, P>(M.csr)
-#define RSEGK(UU, P, MB) (M.csr.ci16 ? k_rseg<UU, P, true, MB> : k_rseg<UU, P, false, MB>)
-#define RSEGPK(UU, P, MB) (M.csr.ci16 ? k_rsegp<UU, P, true, MB> : k_rsegp<UU, P, false, MB>)
-// Row-segment variants (U*10 + min CTAs/SM) instantiated below.
-#define ASPAMG_RSEG_VARIANTS(X) X(8, 4) X(8, 3) X(16, 2) X(4, 6)
-// Pipelined variants (rseg code 1000 + U*10 + min CTAs/SM).
-#define ASPAMG_RSEGP_VARIANTS(X) X(4, 4) X(4, 5) X(8, 2) X(8, 3)
-
 int spmv_grid(const DMat& M) {
     if (M.fmt == 1) {
         const long long ch = (M.sb.nchunks + 7) / 8;
         return M.sb.pol == 1 ? occ_grid(k_sbsr3<1>, ch) : M.sb.pol == 2 ? occ_grid(k_sbsr3<2>, ch) : occ_grid(k_sbsr3<0>, ch);
-    }
-    if (M.fmt == 2 && M.sell.tma) {
-        const long long ch = (M.sell.nchunks + 7) / 8;
-        const bool st = M.sell.pol == 1;
-#define ASPAMG_TMA_OCC(SG, SS)                                                                  \
-    if (M.sell.tma == SG * 10 + SS)                                                             \
-        return st ? occ_grid(k_sell_tma<SG, SS, true>, ch, SellTmaCfg<SG, SS>::kBlockBytes)     \
-                  : occ_grid(k_sell_tma<SG, SS, false>, ch, SellTmaCfg<SG, SS>::kBlockBytes);
-        ASPAMG_TMA_OCC(16, 4)
-        ASPAMG_TMA_OCC(16, 2)
-        ASPAMG_TMA_OCC(8, 4)
-        ASPAMG_TMA_OCC(8, 2)
-        ASPAMG_TMA_OCC(4, 4)
-#undef ASPAMG_TMA_OCC
-        return 1;
     }
     if (M.fmt == 2) {
         const long long ch = (M.sell.nchunks + 7) / 8;
@@ -1309,32 +837,11 @@ int spmv_grid(const DMat& M) {
     if (M.sell.u == UU * 10 + MB)                                                                \
         return st == 1 ? occ_grid(SELLK(UU, 1, MB), ch)                                          \
                        : st == 2 ? occ_grid(SELLK(UU, 2, MB), ch) : occ_grid(SELLK(UU, 0, MB), ch);
-        ASPAMG_SELL_OCC(8, 1)
         ASPAMG_SELL_OCC(8, 3)
-        ASPAMG_SELL_OCC(8, 4)
         ASPAMG_SELL_OCC(4, 1)
         ASPAMG_SELL_OCC(4, 4)
-        ASPAMG_SELL_OCC(4, 6)
         ASPAMG_SELL_OCC(2, 1)
 #undef ASPAMG_SELL_OCC
-        return 1;
-    }
-    if (M.csr.rseg) {
-        const long long wb = ((long long)M.csr.n_rows + 31) / 32;  // 32-row blocks, one per warp
-        const long long ctas = (wb + kBlock / 32 - 1) / (kBlock / 32);
-        const int st = M.csr.pol;
-#define ASPAMG_RSEG_OCC(UU, MB)                                                                   \
-    if (M.csr.rseg == UU * 10 + MB)                                                               \
-        return st == 1 ? occ_grid(RSEGK(UU, 1, MB), ctas)                                         \
-                       : st == 2 ? occ_grid(RSEGK(UU, 2, MB), ctas) : occ_grid(RSEGK(UU, 0, MB), ctas);
-        ASPAMG_RSEG_VARIANTS(ASPAMG_RSEG_OCC)
-#undef ASPAMG_RSEG_OCC
-#define ASPAMG_RSEGP_OCC(UU, MB)                                                                  \
-    if (M.csr.rseg == 1000 + UU * 10 + MB)                                                        \
-        return st == 1 ? occ_grid(RSEGPK(UU, 1, MB), ctas)                                        \
-                       : st == 2 ? occ_grid(RSEGPK(UU, 2, MB), ctas) : occ_grid(RSEGPK(UU, 0, MB), ctas);
-        ASPAMG_RSEGP_VARIANTS(ASPAMG_RSEGP_OCC)
-#undef ASPAMG_RSEGP_OCC
         return 1;
     }
     const int T = M.csr.group;
@@ -1371,25 +878,6 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
             launch(k_sbsr3<0>, grid, kBlock, 0, L.stream, M.sb, epi, x, y, aux, omega, dotw, red, done);
         return;
     }
-    if (M.fmt == 2 && M.sell.tma) {
-#define ASPAMG_SELLT(SG, SS)                                                                                  \
-    if (M.sell.tma == SG * 10 + SS) {                                                                         \
-        if (M.sell.pol == 1)                                                                                  \
-            launch(k_sell_tma<SG, SS, true>, grid, kBlock, SellTmaCfg<SG, SS>::kBlockBytes, L.stream,        \
-                   M.sell, epi, x, y, aux, omega, dotw, red, done);                                              \
-        else                                                                                                  \
-            launch(k_sell_tma<SG, SS, false>, grid, kBlock, SellTmaCfg<SG, SS>::kBlockBytes, L.stream,       \
-                   M.sell, epi, x, y, aux, omega, dotw, red, done);                                              \
-        return;                                                                                               \
-    }
-        ASPAMG_SELLT(16, 4)
-        ASPAMG_SELLT(16, 2)
-        ASPAMG_SELLT(8, 4)
-        ASPAMG_SELLT(8, 2)
-        ASPAMG_SELLT(4, 4)
-#undef ASPAMG_SELLT
-        return;
-    }
     if (M.fmt == 2) {
 #define ASPAMG_SELL(UU, MB)                                                                                          \
     if (M.sell.u == UU * 10 + MB) {                                                                                 \
@@ -1401,41 +889,11 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
             launch(SELLK(UU, 0, MB), grid, kBlock, 0, L.stream, M.sell, epi, x, y, aux, omega, dotw, red, done);      \
         return;                                                                                                     \
     }
-        ASPAMG_SELL(8, 1)
         ASPAMG_SELL(8, 3)
-        ASPAMG_SELL(8, 4)
         ASPAMG_SELL(4, 1)
         ASPAMG_SELL(4, 4)
-        ASPAMG_SELL(4, 6)
         ASPAMG_SELL(2, 1)
 #undef ASPAMG_SELL
-        return;
-    }
-    if (M.csr.rseg) {
-#define ASPAMG_RSEG(UU, MB)                                                                                         \
-    if (M.csr.rseg == UU * 10 + MB) {                                                                              \
-        if (M.csr.pol == 1)                                                                                        \
-            launch(RSEGK(UU, 1, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
-        else if (M.csr.pol == 2)                                                                                   \
-            launch(RSEGK(UU, 2, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
-        else                                                                                                       \
-            launch(RSEGK(UU, 0, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);      \
-        return;                                                                                                    \
-    }
-        ASPAMG_RSEG_VARIANTS(ASPAMG_RSEG)
-#undef ASPAMG_RSEG
-#define ASPAMG_RSEGP(UU, MB)                                                                                        \
-    if (M.csr.rseg == 1000 + UU * 10 + MB) {                                                                       \
-        if (M.csr.pol == 1)                                                                                        \
-            launch(RSEGPK(UU, 1, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);     \
-        else if (M.csr.pol == 2)                                                                                   \
-            launch(RSEGPK(UU, 2, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);     \
-        else                                                                                                       \
-            launch(RSEGPK(UU, 0, MB), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);     \
-        return;                                                                                                    \
-    }
-        ASPAMG_RSEGP_VARIANTS(ASPAMG_RSEGP)
-#undef ASPAMG_RSEGP
         return;
     }
 #define ASPAMG_CSR_CASE(GG)                                                                                   \
@@ -1515,17 +973,6 @@ void spmv_prepare() {
     static bool done = false;
     if (done) return;
     done = true;
-#define ASPAMG_TMA_ATTR(SG, SS)                                                                                      \
-    cudaFuncSetAttribute(k_sell_tma<SG, SS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                      \
-                         SellTmaCfg<SG, SS>::kBlockBytes);                                                           \
-    cudaFuncSetAttribute(k_sell_tma<SG, SS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,                     \
-                         SellTmaCfg<SG, SS>::kBlockBytes);
-    ASPAMG_TMA_ATTR(16, 4)
-    ASPAMG_TMA_ATTR(16, 2)
-    ASPAMG_TMA_ATTR(8, 4)
-    ASPAMG_TMA_ATTR(8, 2)
-    ASPAMG_TMA_ATTR(4, 4)
-#undef ASPAMG_TMA_ATTR
 }
 
 void coarse_prepare(int n) {

@@ -27,16 +27,7 @@ struct DCsr {
     // column = cb[row] + ci16[k] (10 instead of 12 matrix bytes per entry)
     unsigned short* ci16 = nullptr;
     int* cb = nullptr;
-    // Row-segment mode (k_rseg, 0 = off, else U*10 + min CTAs/SM): a warp owns 32
-    // consecutive rows, streams their contiguous CSR segment in tiles of 32*U
-    // entries (every lane loads consecutive entries: no padding, U independent
-    // loads per lane in flight), stages the products v*x in shared memory, and
-    // each lane then sums its own row in ascending column order. With 16-bit
-    // offsets cb holds one base column per 32-row block (not per row).
-    int rseg = 0;
-    int u8 = 0;  // k_csr with 8 loads per thread per round (1: T >= 32, 2: every T)
     int pf = 0;  // k_csr row-pointer prefetch (T <= 16)
-    int vec = 0;  // k_csrv: quad-vectorized loads (16-bit offsets, T >= 16)
     // Long-row split: rows longer than lthr (listed in lrows) are computed by the
     // first nlctas CTAs of the launch, one warp per row; the regular T-thread
     // groups skip them, so a long-tailed operand (G' rows up to ~7x the mean) no
@@ -75,7 +66,6 @@ struct DSell {
     int* perm = nullptr;  // SELL-32-sigma: slot row -> matrix row (null = natural order)
     int* len = nullptr;   // per slot row
     int u = 81;           // register-pipelined variant: U*10 + min CTAs/SM (81, 83, 84, 41, 44, 46, 21)
-    int tma = 0;          // 0: register pipeline; SEG*10+S: TMA-staged ring (164, 162, 84, 82, 44)
     int2* meta = nullptr;
     int* ci = nullptr;
     double* v = nullptr;

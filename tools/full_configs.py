@@ -47,7 +47,7 @@ def main():
     threads = os.cpu_count() or 1
     for cfg in args.configs:
         t0 = time.perf_counter()
-        prob, h, t_gen, t_setup = bench.get_hierarchy(P, cfg, args.scale, 0, D(), threads,
+        prob, h, t_gen, t_setup, _origin = bench.get_hierarchy(P, cfg, args.scale, 0, D(), threads,
                                                       0 if args.gpu_setup else None)
         info = h.info()
         print(cfg, "setup", round(t_gen, 1), round(t_setup, 1), {k: round(getattr(info, k), 2) for k in

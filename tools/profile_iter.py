@@ -27,7 +27,7 @@ def main():
         def barrier(self):
             pass
 
-    prob, h, _, _ = bench.get_hierarchy(P, args.config, args.scale, 0, D(), os.cpu_count() or 1)
+    prob, h, _, _, _ = bench.get_hierarchy(P, args.config, args.scale, 0, D(), os.cpu_count() or 1)
     opts = {k: int(v) for k, v in (o.split("=") for o in args.opt)}
     g = P.GpuVcycle(h, device=0, options=opts)
     # ncu runs this with --profile-from-start off: only the two body runs below are

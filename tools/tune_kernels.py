@@ -45,7 +45,7 @@ def main():
         def barrier(self):
             pass
 
-    prob, h, _, _ = bench.get_hierarchy(P, args.config, args.scale, 0, D(), os.cpu_count() or 1)
+    prob, h, _, _, _ = bench.get_hierarchy(P, args.config, args.scale, 0, D(), os.cpu_count() or 1)
     res = {}
     for name, opts in sets.items():
         g = P.GpuVcycle(h, device=0, options=opts)
