@@ -17,6 +17,7 @@
 
 #include <array>
 #include <cstdint>
+#include <cstring>
 #include <memory>
 #include <optional>
 #include <span>
@@ -195,6 +196,7 @@ public:
     ~GpuVcycle() { aspamg_gpu_ctx_destroy(ctx_); }
 
     index_t size() const { return n_; }
+    const Hierarchy& hierarchy() const { return *h_; }
     // vcycle_apply(h, y)
     std::vector<double> operator()(std::span<const double> y) const {
         if (static_cast<index_t>(y.size()) != n_) throw DimensionError("vcycle_apply: y length mismatch");
@@ -238,13 +240,29 @@ private:
 
 inline std::vector<double> vcycle_apply(const GpuVcycle& h, std::span<const double> y) { return h(y); }
 
-// SPEC.md:504-512. A must be the finest operator of `precond` (it lives on the device).
+// True when two CSR views hold the same matrix (same sizes, same arrays bit for
+// bit); borrowed views of one buffer compare by pointer.
+inline bool same_matrix(const aspamg_csr_view& a, const aspamg_csr_view& b) {
+    if (a.n_rows != b.n_rows || a.n_cols != b.n_cols || a.nnz != b.nnz) return false;
+    auto eq = [](const void* p, const void* q, size_t bytes) {
+        return p == q || bytes == 0 || std::memcmp(p, q, bytes) == 0;
+    };
+    return eq(a.row_offsets, b.row_offsets, sizeof(int64_t) * static_cast<size_t>(a.n_rows + 1)) &&
+           eq(a.col_indices, b.col_indices, sizeof(int64_t) * static_cast<size_t>(a.nnz)) &&
+           eq(a.values, b.values, sizeof(double) * static_cast<size_t>(a.nnz));
+}
+
+// SPEC.md:504-512. The Krylov operator lives on the device as the finest level
+// of `precond`'s hierarchy, so A must be that matrix: a different A of the same
+// size (e.g. a stale cached hierarchy) would silently solve another system.
 inline std::pair<std::vector<double>, SolveReport> pcg(const SparseMatrix& A, std::span<const double> b,
                                                        const GpuVcycle& precond, double rel_tol = 1e-8,
                                                        index_t max_it = 1000,
                                                        const std::vector<double>* x0 = nullptr) {
     if (A.n_rows != A.n_cols || A.n_rows != precond.size())
         throw DimensionError("pcg: operator does not match the preconditioner's finest level");
+    if (!same_matrix(A.view(), precond.hierarchy().level(0).A))
+        throw DimensionError("pcg: A differs from the finest operator of the preconditioner's hierarchy");
     return precond.solve(b, rel_tol, max_it, x0);
 }
 

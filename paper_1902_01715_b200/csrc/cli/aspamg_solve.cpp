@@ -163,7 +163,12 @@ int main(int argc, char** argv) {
         std::optional<Hierarchy> h;
         if (!hier_path.empty()) {
             std::ifstream probe(hier_path);
-            if (probe) h.emplace(Hierarchy::load(hier_path));
+            if (probe) {
+                h.emplace(Hierarchy::load(hier_path));
+                // a cached hierarchy must have been built from this very matrix
+                if (!same_matrix(A.view(), h->level(0).A))
+                    throw ConfigError("--hierarchy " + hier_path + " was built from a different matrix");
+            }
         }
         if (!h) {
             h.emplace(amg_setup(A, xyz, cfg));

@@ -58,11 +58,23 @@ void check_view(const aspamg_csr_view* v, const char* what) {
     if (v->n_rows > 0 && v->row_offsets[v->n_rows] != v->nnz) throw Fail{1, std::string(what) + ": nnz mismatch"};
     if (v->nnz >= (1ll << 31) || v->n_rows >= (1ll << 31) || v->n_cols >= (1ll << 31))
         throw Fail{4, std::string(what) + ": exceeds int32 device indexing"};
+    // Columns in range and strictly ascending within each row (the SparseMatrix
+    // invariant, sparse_matrix.hpp:27-33): the 16-bit column mode stores
+    // col - first-col-of-row and would wrap on an unsorted row.
     int bad = 0;
-#pragma omp parallel for schedule(static) reduction(| : bad)
-    for (int64_t k = 0; k < v->nnz; ++k)
-        bad |= (v->col_indices[k] < 0 || v->col_indices[k] >= v->n_cols);
-    if (bad) throw Fail{1, std::string(what) + ": column index out of range"};
+#pragma omp parallel for schedule(dynamic, 4096) reduction(| : bad)
+    for (int64_t i = 0; i < v->n_rows; ++i) {
+        const int64_t b = v->row_offsets[i], e = v->row_offsets[i + 1];
+        if (b > e || b < 0 || e > v->nnz) { bad |= 2; continue; }
+        for (int64_t k = b; k < e; ++k) {
+            const int64_t c = v->col_indices[k];
+            bad |= (c < 0 || c >= v->n_cols);
+            if (k > b && c <= v->col_indices[k - 1]) bad |= 4;
+        }
+    }
+    if (bad & 2) throw Fail{1, std::string(what) + ": row offsets not monotone"};
+    if (bad & 1) throw Fail{1, std::string(what) + ": column index out of range"};
+    if (bad & 4) throw Fail{1, std::string(what) + ": column indices not strictly ascending within a row"};
 }
 
 // Threads per row for the CSR kernel: ~4+ entries per thread, widened for

@@ -87,12 +87,14 @@ class SparseMatrix:
         return int(self.col_indices.shape[0])
 
     @classmethod
-    def from_view(cls, v: N.CsrView, copy: bool = True) -> "SparseMatrix":
+    def from_view(cls, v: N.CsrView, copy: bool = True, owner=None) -> "SparseMatrix":
+        """copy=False borrows the native buffers; ``owner`` (the object whose
+        lifetime bounds them) is then kept alive by every array."""
         if v.n_rows == 0 and v.nnz == 0 and not v.row_offsets:
             return cls(0, int(v.n_cols), np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
-        rp = np.ctypeslib.as_array(v.row_offsets, shape=(v.n_rows + 1,))
-        ci = np.ctypeslib.as_array(v.col_indices, shape=(v.nnz,)) if v.nnz else np.zeros(0, np.int64)
-        va = np.ctypeslib.as_array(v.values, shape=(v.nnz,)) if v.nnz else np.zeros(0)
+        rp = _borrow(v.row_offsets, (v.n_rows + 1,), owner)
+        ci = _borrow(v.col_indices, (v.nnz,), owner) if v.nnz else np.zeros(0, np.int64)
+        va = _borrow(v.values, (v.nnz,), owner) if v.nnz else np.zeros(0)
         if copy:
             rp, ci, va = rp.copy(), ci.copy(), va.copy()
         return cls(int(v.n_rows), int(v.n_cols), rp, ci, va)
@@ -116,6 +118,21 @@ class SparseMatrix:
                          _ptr(self.col_indices, C.c_int64), _ptr(self.values, C.c_double))
 
 
+class _Borrowed:
+    """Array-interface wrapper: a numpy view of native memory whose base holds
+    the memory's owner, so `K = Problem.config(2).K` cannot outlive its buffers."""
+
+    def __init__(self, arr: np.ndarray, owner):
+        self.__array_interface__ = arr.__array_interface__
+        self._arr = arr
+        self._owner = owner
+
+
+def _borrow(ptr, shape, owner) -> np.ndarray:
+    a = np.ctypeslib.as_array(ptr, shape=shape)
+    return a if owner is None else np.asarray(_Borrowed(a, owner))
+
+
 # ------------------------------------------------------------------ problem
 class Problem:
     """Generated elasticity problem (fem.hpp:43-66 restated; BASELINE configs 1-5)."""
@@ -125,14 +142,14 @@ class Problem:
         lib = N.host()
         v = N.CsrView()
         _chk_host(lib.aspamg_problem_matrix(self._h, C.byref(v)))
-        self.K = SparseMatrix.from_view(v, copy=False)
+        self.K = SparseMatrix.from_view(v, copy=False, owner=self)
         self.K.symmetric = True
         rp = N.P_dbl()
         n = C.c_int64()
         _chk_host(lib.aspamg_problem_rhs(self._h, C.byref(rp), C.byref(n)))
-        self.rhs = np.ctypeslib.as_array(rp, shape=(n.value,)) if n.value else np.zeros(0)
+        self.rhs = _borrow(rp, (n.value,), self) if n.value else np.zeros(0)
         _chk_host(lib.aspamg_problem_coords(self._h, C.byref(rp), C.byref(n)))
-        self.coords = np.ctypeslib.as_array(rp, shape=(n.value, 3)) if n.value else np.zeros((0, 3))
+        self.coords = _borrow(rp, (n.value, 3), self) if n.value else np.zeros((0, 3))
 
     @classmethod
     def config(cls, cfg: int, scale: int = 1) -> "Problem":
@@ -244,7 +261,7 @@ class Hierarchy:
 
     def level(self, l: int, copy: bool = True) -> LevelData:
         lv = self.level_view(l)
-        f = lambda v: SparseMatrix.from_view(v, copy)  # noqa: E731
+        f = lambda v: SparseMatrix.from_view(v, copy, None if copy else self)  # noqa: E731
         return LevelData(f(lv.A), f(lv.G), f(lv.Gt), f(lv.P), f(lv.Pt), lv.omega, lv.lambda_hat,
                          int(lv.refinement_passes), int(lv.smoother_exit), int(lv.n_tv), float(lv.t_smoother))
 
@@ -570,6 +587,13 @@ def vcycle_apply(h: GpuVcycle, y: np.ndarray) -> np.ndarray:
     return h.apply(y)
 
 
+def _same_matrix(a: SparseMatrix, b: SparseMatrix) -> bool:
+    if (a.n_rows, a.n_cols, a.nnz) != (b.n_rows, b.n_cols, b.nnz):
+        return False
+    return all(x is y or x.ctypes.data == y.ctypes.data or np.array_equal(x, y)
+               for x, y in ((a.row_offsets, b.row_offsets), (a.col_indices, b.col_indices), (a.values, b.values)))
+
+
 def pcg(A: SparseMatrix, b: np.ndarray, precond: GpuVcycle, rel_tol: float = 1e-8, max_it: int = 1000,
         x0: Optional[np.ndarray] = None) -> tuple[np.ndarray, SolveReport]:
     """SPEC.md:504-512. The operator A must be the finest level of ``precond``'s
@@ -578,5 +602,8 @@ def pcg(A: SparseMatrix, b: np.ndarray, precond: GpuVcycle, rel_tol: float = 1e-
     converged=False."""
     if A.n_rows != precond.n or A.n_cols != precond.n:
         raise DimensionError("pcg: operator does not match the preconditioner's finest level")
+    if not _same_matrix(A, precond.hierarchy.level(0, copy=False).A):
+        # the Krylov operator on the device is the hierarchy's level 0, not A
+        raise DimensionError("pcg: A differs from the finest operator of the preconditioner's hierarchy")
     x, rep = precond.pcg(b, x0=x0, rel_tol=rel_tol, max_it=max_it)
     return x, rep

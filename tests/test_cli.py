@@ -24,6 +24,30 @@ def test_cli_exit_codes(tmp_path):
     assert run("--matrix", str(bad)).returncode == 2
 
 
+def _write_mtx(path, K):
+    K = K.tocoo()
+    low = K.row >= K.col
+    with open(path, "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real symmetric\n% generated\n")
+        f.write(f"{K.shape[0]} {K.shape[1]} {int(low.sum())}\n")
+        for i, j, v in zip(K.row[low], K.col[low], K.data[low]):
+            f.write(f"{i + 1} {j + 1} {float(v)!r}\n")
+
+
+def test_cli_rejects_stale_hierarchy(tmp_path, pkg):
+    """--hierarchy must not reuse a cache built from another matrix of the same size
+    (the device Krylov operator is the hierarchy's level 0, not the input A)."""
+    p = pkg.Problem.hex_cube(3, spacing=1 / 3)
+    K = p.K.to_scipy()
+    hb = tmp_path / "h.bin"
+    _write_mtx(tmp_path / "K.mtx", K)
+    run("--matrix", str(tmp_path / "K.mtx"), "--hierarchy", str(hb))  # builds + saves (solve needs a GPU)
+    assert hb.exists()
+    _write_mtx(tmp_path / "K2.mtx", 2.0 * K)
+    r = run("--matrix", str(tmp_path / "K2.mtx"), "--hierarchy", str(hb))
+    assert r.returncode == 1 and "different matrix" in r.stderr
+
+
 def _has_gpu():
     import ctypes as C
     import sys
@@ -55,17 +79,23 @@ def test_cli_solve_matches_python_api(tmp_path, pkg):
 
 
 @pytest.mark.gpu
+def test_pcg_rejects_foreign_operator(pkg):
+    """pcg(A, b, M): A of the right size but not M's finest operator -> DimensionError."""
+    p = pkg.Problem.config(1, 4)
+    M = pkg.GpuVcycle(pkg.Hierarchy.setup(p.K, p.coords))
+    K2 = pkg.SparseMatrix(p.K.n_rows, p.K.n_cols, p.K.row_offsets.copy(), p.K.col_indices.copy(), 2.0 * p.K.values)
+    with pytest.raises(pkg.DimensionError):
+        pkg.pcg(K2, p.rhs, M)
+    x, rep = pkg.pcg(p.K, p.rhs, M)
+    assert rep.converged
+
+
+@pytest.mark.gpu
 def test_cli_matrix_market_input(tmp_path, pkg):
     """symmetric Matrix Market (lower triangle) + coordinates, ones rhs."""
     p = pkg.Problem.hex_cube(4, spacing=0.25)
-    K = p.K.to_scipy().tocoo()
-    low = K.row >= K.col
     mtx = tmp_path / "K.mtx"
-    with open(mtx, "w") as f:
-        f.write("%%MatrixMarket matrix coordinate real symmetric\n% generated\n")
-        f.write(f"{K.shape[0]} {K.shape[1]} {int(low.sum())}\n")
-        for i, j, v in zip(K.row[low], K.col[low], K.data[low]):
-            f.write(f"{i + 1} {j + 1} {float(v)!r}\n")
+    _write_mtx(mtx, p.K.to_scipy())
     xyz = tmp_path / "xyz.txt"
     np.savetxt(xyz, p.coords)
     r = run("--matrix", str(mtx), "--coords", str(xyz))

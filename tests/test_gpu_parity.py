@@ -390,3 +390,22 @@ def test_sell_all_empty_row_groups(pkg):
         assert np.array_equal(y, Pm @ x)
     finally:
         lib.aspamg_gpu_ctx_destroy(ctx)
+
+
+def test_upload_rejects_unsorted_row(pkg):
+    """check_view: columns must ascend within a row (sparse_matrix.hpp:27-33) —
+    the 16-bit column mode would otherwise wrap silently. Status 1 (DimensionError)."""
+    import ctypes as C
+    from paper_1902_01715_b200 import _native as N
+    lib = N.gpu()
+    ctx = C.c_void_p()
+    assert lib.aspamg_gpu_ctx_create(0, C.byref(ctx)) == 0
+    A = pkg.SparseMatrix(3, 3, np.array([0, 2, 3, 5], np.int64), np.array([1, 0, 1, 0, 2], np.int64),
+                         np.array([1.0, 4.0, 4.0, 1.0, 4.0]))
+    e = pkg.SparseMatrix(0, 0, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    v = A.view()
+    ev = e.view()
+    code = lib.aspamg_gpu_upload_level(ctx, 0, C.byref(v), C.byref(ev), C.byref(ev), C.byref(ev), C.byref(ev), 1.0)
+    assert code == 1
+    assert b"ascending" in lib.aspamg_gpu_last_error(ctx)
+    lib.aspamg_gpu_ctx_destroy(ctx)
