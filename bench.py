@@ -423,7 +423,7 @@ def run_b200(args, ws, rank, local):
     if rank != 0:
         return 0
     lv0 = g.level_info(0)
-    fmts = {0: "csr", 1: "sbsr3", 2: "sell", -1: None}
+    fmts = {0: "csr", 1: "sbsr3", 2: "sell", 3: "xsell", -1: None}
     levels = []
     for l in range(int(info.n_levels)):
         li = g.level_info(l)

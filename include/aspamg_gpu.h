@@ -145,6 +145,13 @@ int aspamg_gpu_set_setup_policy(const char* key, double value);
 int aspamg_gpu_afsai_build(void* device, const aspamg_csr_view* A, int64_t k, int64_t rho, double eps,
                            aspamg_csr_alloc_fn alloc, void* sink, double* psi);
 
+/* Layout self-check of the tile-local SELL format ("xsell") — host only, no
+ * device needed: builds the format's arrays for A exactly as upload does and walks them on
+ * the CPU with the kernel's indexing (staged x window, 16-bit local columns, quads, tile
+ * permutation). y must equal spmv(A, x) (sparse_matrix.cpp:96-107) bit for bit. */
+int aspamg_gpu_xsell_layout_spmv(const aspamg_csr_view* A, int64_t tile_rows, int64_t fold, int64_t gran,
+                                 const double* x, double* y);
+
 /* measurement helpers */
 int aspamg_gpu_last_solve_ms(aspamg_gpu_ctx* ctx, double* ms);      /* device time of the last pcg */
 int aspamg_gpu_launch_count(aspamg_gpu_ctx* ctx, int64_t* n);       /* kernels launched by the last pcg */

@@ -162,6 +162,7 @@ def gpu() -> C.CDLL:
         lib.aspamg_gpu_launch_count.argtypes = [vp, P_i64]
         lib.aspamg_gpu_last_solve_ms.argtypes = [vp, P_dbl]
         lib.aspamg_gpu_stream.argtypes = [vp, C.POINTER(vp)]
+        lib.aspamg_gpu_xsell_layout_spmv.argtypes = [C.POINTER(CsrView), i64, i64, i64, P_dbl, P_dbl]
         lib.aspamg_gpu_srqcg.argtypes = [vp, C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(CsrView), P_dbl, i64, i64,
                                          i64, dbl, C.c_uint64, P_dbl, P_dbl, P_i64, P_i64, C.POINTER(C.c_int)]
         lib.aspamg_gpu_galerkin.argtypes = [vp, C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(CsrView), vp, vp]

@@ -126,7 +126,226 @@ bool rows_fit_u16(const aspamg_csr_view& v) {
     return ok != 0;
 }
 
-DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
+// Tile-local SELL build (layout in kernels.cuh, DXsell), host side. Returns
+// false when the operand does not fit the format (a tile's x footprint larger
+// than the shared-memory budget, a row longer than 65535 entries).
+struct XsellHost {
+    int R = 0, F = 1, g = 0, fp_doubles = 0;
+    int64_t nt = 0;
+    long long quads = 0, list_len = 0;
+    std::vector<unsigned short> slen, perm;
+    std::vector<int2> tmeta, cmeta;
+    std::vector<int> list;
+    std::vector<double2> val;
+    std::vector<uint2> lc;
+};
+
+// Slot (chunk, lane, part) of sorted rank i inside a tile of R rows: fold 1 ->
+// chunk i / 32, lane i % 32, part a; fold 2 -> ranks < R/2 are the a rows of
+// thread i, ranks >= R/2 the b rows of thread R-1-i.
+struct XsellSlot {
+    int chunk, lane, part;
+};
+inline XsellSlot xsell_slot(int i, int R, int F) {
+    if (F == 1 || i < R / 2) return {i / 32, i % 32, 0};
+    const int t = R - 1 - i;
+    return {t / 32, t % 32, 1};
+}
+
+bool build_xsell_host(const aspamg_csr_view& v, int R, int F, int g, size_t cap_doubles, XsellHost& H) {
+    const int64_t n = v.n_rows;
+    if (n <= 0 || v.nnz <= 0) return false;
+    const int64_t nt = (n + R - 1) / R;
+    const int cpt = R / F / 32;  // chunks (warps) per tile
+    H.F = F;
+    if (nt * cpt >= (1ll << 30)) return false;
+    H.R = R;
+    H.g = g;
+    H.nt = nt;
+    H.slen.assign((size_t)(nt * R), 0);
+    H.perm.assign((size_t)(nt * R), 0);
+    std::vector<int> cw((size_t)(nt * cpt), 0), cwb((size_t)(nt * cpt), 0);
+    std::vector<std::vector<int>> fp((size_t)nt);
+    int too_big = 0;
+#pragma omp parallel
+    {
+        std::vector<int> ord((size_t)R), gl;
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t t = 0; t < nt; ++t) {
+            const int64_t r0 = t * R, r1 = std::min<int64_t>(n, r0 + R);
+            const int m = (int)(r1 - r0);
+            auto rlen = [&](int i) { return v.row_offsets[r0 + i + 1] - v.row_offsets[r0 + i]; };
+            for (int i = 0; i < R; ++i) ord[(size_t)i] = i;
+            std::stable_sort(ord.begin(), ord.begin() + m, [&](int a, int b) { return rlen(a) > rlen(b); });
+            for (int i = 0; i < R; ++i) {
+                H.perm[(size_t)(r0 + i)] = (unsigned short)ord[(size_t)i];
+                const int64_t li = i < m ? rlen(ord[(size_t)i]) : 0;
+                if (li > 65535) {
+#pragma omp atomic write
+                    too_big = 1;
+                }
+                H.slen[(size_t)(r0 + i)] = (unsigned short)std::min<int64_t>(li, 65535);
+            }
+            for (int w = 0; w < cpt; ++w) {  // sorted: the smallest rank of a chunk part is its longest row
+                cw[(size_t)(t * cpt + w)] = H.slen[(size_t)(r0 + 32 * w)];
+                if (F == 2) cwb[(size_t)(t * cpt + w)] = H.slen[(size_t)(r0 + R - 32 * w - 32)];
+            }
+            gl.clear();
+            for (int64_t k = v.row_offsets[r0]; k < v.row_offsets[r1]; ++k) gl.push_back((int)(v.col_indices[k] >> g));
+            std::sort(gl.begin(), gl.end());
+            gl.erase(std::unique(gl.begin(), gl.end()), gl.end());
+            if (((size_t)gl.size() << g) > cap_doubles || ((size_t)gl.size() << g) > 65536) {
+#pragma omp atomic write
+                too_big = 1;
+            }
+            fp[(size_t)t] = gl;
+        }
+    }
+    if (too_big) return false;
+    H.tmeta.resize((size_t)nt);
+    H.cmeta.resize((size_t)(nt * cpt));
+    long long lo = 0, qo = 0;
+    size_t maxfp = 0;
+    for (int64_t t = 0; t < nt; ++t) {
+        H.tmeta[(size_t)t] = make_int2((int)lo, (int)fp[(size_t)t].size());
+        lo += (long long)fp[(size_t)t].size();
+        maxfp = std::max(maxfp, fp[(size_t)t].size());
+        for (int w = 0; w < cpt; ++w) {
+            const int wd = cw[(size_t)(t * cpt + w)], wb = cwb[(size_t)(t * cpt + w)];
+            H.cmeta[(size_t)(t * cpt + w)] = make_int2((int)qo, wd | (wb << 16));
+            qo += (wd + 3) / 4 + (wb + 3) / 4;
+        }
+        if (lo > INT_MAX - 65536 || qo > INT_MAX / 64 - 65536) return false;
+    }
+    H.list.resize((size_t)std::max<long long>(lo, 1));
+    H.val.assign((size_t)std::max<long long>(qo, 1) * 64, make_double2(0.0, 0.0));
+    H.lc.assign((size_t)std::max<long long>(qo, 1) * 32, make_uint2(0u, 0u));
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t t = 0; t < nt; ++t) {
+        const std::vector<int>& gl = fp[(size_t)t];
+        std::copy(gl.begin(), gl.end(), H.list.begin() + H.tmeta[(size_t)t].x);
+        const int64_t r0 = t * R, r1 = std::min<int64_t>(n, r0 + R);
+        for (int i = 0; i < (int)(r1 - r0); ++i) {
+            const int64_t row = r0 + H.perm[(size_t)(r0 + i)];
+            const XsellSlot sl = xsell_slot(i, R, F);
+            const int2 cmw = H.cmeta[(size_t)(t * cpt + sl.chunk)];
+            const long long q0 = cmw.x + (sl.part ? ((cmw.y & 0xffff) + 3) / 4 : 0);
+            const int lane = sl.lane;
+            const int64_t b = v.row_offsets[row], e = v.row_offsets[row + 1];
+            for (int64_t k = b; k < e; ++k) {
+                const int j = (int)(k - b);
+                const int64_t col = v.col_indices[k];
+                const int rank = (int)(std::lower_bound(gl.begin(), gl.end(), (int)(col >> g)) - gl.begin());
+                const unsigned loc = ((unsigned)rank << g) | (unsigned)(col & ((1 << g) - 1));
+                const long long q = q0 + j / 4;
+                double2& dv = H.val[(size_t)((q * 2 + (j % 4) / 2) * 32 + lane)];
+                if (j % 2 == 0) dv.x = v.values[k];
+                else dv.y = v.values[k];
+                uint2& dc = H.lc[(size_t)(q * 32 + lane)];
+                unsigned& w = (j % 4) < 2 ? dc.x : dc.y;
+                w |= (j % 2 == 0) ? loc : (loc << 16);
+            }
+        }
+    }
+    H.quads = qo;
+    H.list_len = lo;
+    H.fp_doubles = (int)(((maxfp << g) + 1) / 2 * 2);
+    return true;
+}
+
+// CPU walk of the layout exactly as k_xsell indexes it (staged window, quads,
+// per-lane sequential sums, output through the tile permutation): the layout
+// check that runs without a GPU (tests/test_abi.py).
+void xsell_host_spmv(const XsellHost& H, int64_t n_rows, int64_t n_cols, const double* x, double* y) {
+    const int R = H.R, F = H.F, g = H.g, cpt = R / F / 32;
+#pragma omp parallel
+    {
+        std::vector<double> win((size_t)H.fp_doubles + 2), ys((size_t)R);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t t = 0; t < H.nt; ++t) {
+            const int2 tm = H.tmeta[(size_t)t];
+            for (int q = 0; q < tm.y; ++q)
+                for (int o = 0; o < (1 << g); ++o) {
+                    const int64_t i = ((int64_t)H.list[(size_t)(tm.x + q)] << g) + o;
+                    win[(size_t)((q << g) + o)] = i < n_cols ? x[i] : 0.0;
+                }
+            for (int i = 0; i < R; ++i) {
+                const int64_t srow = t * R + i;
+                const int len = H.slen[(size_t)srow];
+                const XsellSlot sl = xsell_slot(i, R, F);
+                const int2 cm = H.cmeta[(size_t)(t * cpt + sl.chunk)];
+                const long long qb = cm.x + (sl.part ? ((cm.y & 0xffff) + 3) / 4 : 0);
+                const int lane = sl.lane;
+                double s = 0.0;
+                for (int j = 0; j < len; ++j) {
+                    const long long q = qb + j / 4;
+                    const double2 dv = H.val[(size_t)((q * 2 + (j % 4) / 2) * 32 + lane)];
+                    const uint2 dc = H.lc[(size_t)(q * 32 + lane)];
+                    const unsigned w = (j % 4) < 2 ? dc.x : dc.y;
+                    const unsigned loc = (j % 2 == 0) ? (w & 0xffffu) : (w >> 16);
+                    const double prod = ((j % 2 == 0) ? dv.x : dv.y) * win[loc];
+                    s = s + prod;
+                }
+                ys[(size_t)H.perm[(size_t)srow]] = s;
+            }
+            for (int tid = 0; tid < R; ++tid)
+                if (t * R + tid < n_rows) y[t * R + tid] = ys[(size_t)tid];
+        }
+    }
+}
+
+// Threads per CTA: "xsell_rows" when set, else by operand size (256 / 128 / 64)
+// so that mid-size operands still spread over all SMs.
+int xsell_threads(const aspamg_gpu_ctx* c, int64_t n) {
+    int T = (int)c->opt_xsell_rows;
+    if (T <= 0) T = n >= c->opt_xsell_rows256 ? 256 : n >= c->opt_xsell_rows128 ? 128 : 64;
+    return std::clamp(T / 32 * 32, 32, kBlock);
+}
+
+bool build_xsell(aspamg_gpu_ctx* c, const aspamg_csr_view& v, DXsell& X) {
+    const int g = (int)std::clamp<long long>(c->opt_xsell_gran, 1, 4);
+    const int F = c->opt_xsell_fold == 2 ? 2 : 1;
+    int T = xsell_threads(c, v.n_rows);
+    XsellHost H;
+    // a tile's footprint must fit the shared-memory budget: halve the tile until it does
+    for (;; T /= 2) {
+        if (T < 32) return false;
+        const int R = T * F;
+        const size_t cap_doubles = (size_t)std::max<long long>(c->opt_xsell_smem_kb, 8) * 128 - (size_t)R;
+        H = XsellHost{};
+        if (build_xsell_host(v, R, F, g, cap_doubles, H)) break;
+    }
+    const int R = T * F;
+    X.n_rows = (int)v.n_rows;
+    X.n_cols = (int)v.n_cols;
+    X.ntiles = (int)H.nt;
+    X.R = R;
+    X.fold = F;
+    X.gran = g;
+    X.nnz = v.nnz;
+    X.quads = H.quads;
+    X.list_len = H.list_len;
+    X.fp_doubles = H.fp_doubles;
+    auto up = [&](auto*& dst, const auto& src) {
+        using T = typename std::remove_reference<decltype(src)>::type::value_type;
+        dst = dalloc<T>(c, src.size());
+        CK(cudaMemcpy(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+    };
+    up(X.tmeta, H.tmeta);
+    up(X.cmeta, H.cmeta);
+    up(X.len, H.slen);
+    up(X.perm, H.perm);
+    up(X.list, H.list);
+    up(X.v, H.val);
+    up(X.lc, H.lc);
+    X.pol = (long long)(10.0 * v.nnz) > c->opt_stream_bytes ? 1 : 0;
+    X.q = c->opt_xsell_q > 0 ? (int)c->opt_xsell_q : 24;
+    xsell_prepare(X);
+    CK(cudaGetLastError());
+    return true;
+}
+
+DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr, int role) {
     DMat M;
     const long long nnz = v.nnz;
     const bool bsr = allow_bsr && c->opt_bsr && exact_bsr3(v);
@@ -173,6 +392,11 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
     for (int64_t i = 0; i < v.n_rows; ++i) {
         len[(size_t)i] = (int)(v.row_offsets[i + 1] - v.row_offsets[i]);
         maxlen = std::max(maxlen, len[(size_t)i]);
+    }
+    if (role >= 0 && ((c->opt_xsell >> role) & 1) && v.n_rows >= c->opt_xsell_min_rows &&
+        mean <= (double)c->opt_xsell_max_mean && build_xsell(c, v, M.xs)) {
+        M.fmt = 3;
+        return M;
     }
     bool sell = v.n_rows >= c->opt_sell_min_rows && mean <= (double)c->opt_sell_max_mean &&
                 mean >= (double)c->opt_sell_min_mean && maxlen <= c->opt_sell_max_len;
@@ -332,6 +556,9 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr) {
 
 // Device bytes of an operand's matrix stream (what one product reads).
 double mat_bytes(const DMat& M) {
+    if (M.fmt == 3)  // padded quads are predicated off: ~10 B per entry + per-row and per-tile metadata
+        return 10.0 * double(M.xs.nnz) + 4.0 * double(M.xs.ntiles) * M.xs.R + 4.0 * double(M.xs.list_len) +
+               8.0 * double(M.xs.ntiles) * (1 + M.xs.R / 32);
     if (M.fmt == 1) return 76.0 * 32.0 * double(M.sb.slots) + 4.0 * M.sb.nb;
     if (M.fmt == 2) return (M.sell.ci16 ? 10.0 : 12.0) * 32.0 * double(M.sell.slots) + (M.sell.ci16 ? 8.0 : 4.0) * M.sell.n_rows;
     const double nb = double(M.csr.n_rows);
@@ -339,12 +566,14 @@ double mat_bytes(const DMat& M) {
 }
 void set_pol(DMat& M, int pol) {
     if (M.fmt == 1) M.sb.pol = pol;
+    else if (M.fmt == 3) M.xs.pol = pol;
     else if (M.fmt == 2) M.sell.pol = pol;
     else M.csr.pol = pol;
 }
 
 // Stored (padded) entries / true nnz of an operand.
 double fill_ratio(const DMat& M) {
+    if (M.fmt == 3) return M.xs.nnz ? double(M.xs.quads) * 128.0 / double(M.xs.nnz) : 1.0;
     if (M.fmt == 1) return M.sb.nnzb ? double(M.sb.slots) * 32.0 / double(M.sb.nnzb) : 1.0;
     if (M.fmt == 2) return M.sell.nnz ? double(M.sell.slots) * 32.0 / double(M.sell.nnz) : 1.0;
     return 1.0;
@@ -357,6 +586,11 @@ double alg_bytes(const DMat& M) {
         const double nnzb = double(M.sb.nnzb);
         return 72.0 * nnzb + 4.0 * nnzb + 4.0 * (M.sb.nb + 1) + 8.0 * M.cols() + 8.0 * M.rows();
     }
+    if (M.fmt == 3) {
+        // values + 16-bit local columns, per-row length + position (2 x 2 B), the footprint lists, x and y once
+        const double nnz = double(M.xs.nnz);
+        return 8.0 * nnz + 2.0 * nnz + 4.0 * M.rows() + 4.0 * double(M.xs.list_len) + 8.0 * M.cols() + 8.0 * M.rows();
+    }
     const double nnz = double(M.fmt == 2 ? M.sell.nnz : M.csr.nnz);
     const bool i16 = M.fmt == 2 ? M.sell.ci16 != nullptr : M.csr.ci16 != nullptr;
     // 16-bit offsets: 2 B per entry + a 4-B base column per row
@@ -367,6 +601,7 @@ double alg_bytes(const DMat& M) {
 
 std::string fmt_name(const DMat& M) {
     const bool h = M.fmt == 2 ? M.sell.ci16 != nullptr : M.fmt == 0 && M.csr.ci16 != nullptr;
+    if (M.fmt == 3) return "xsell" + std::to_string(M.xs.R) + (M.xs.fold == 2 ? "f" : "");
     const std::string base = M.fmt == 1   ? "sbsr3"
                              : M.fmt == 2 ? (M.sell.perm ? "sells" : M.sell.chh == 8 ? "sell8" : "sell")
                                           : "csr" + std::to_string(M.csr.group);
@@ -861,6 +1096,16 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "sell_chh") c->opt_sell_chh = value;
         else if (k == "sell_sort") c->opt_sell_sort = value;
         else if (k == "sell_min_mean") c->opt_sell_min_mean = value;
+        else if (k == "xsell") c->opt_xsell = value;
+        else if (k == "xsell_min_rows") c->opt_xsell_min_rows = value;
+        else if (k == "xsell_max_mean") c->opt_xsell_max_mean = value;
+        else if (k == "xsell_rows") c->opt_xsell_rows = value;
+        else if (k == "xsell_fold") c->opt_xsell_fold = value;
+        else if (k == "xsell_rows256") c->opt_xsell_rows256 = value;
+        else if (k == "xsell_rows128") c->opt_xsell_rows128 = value;
+        else if (k == "xsell_gran") c->opt_xsell_gran = value;
+        else if (k == "xsell_q") c->opt_xsell_q = value;
+        else if (k == "xsell_smem_kb") c->opt_xsell_smem_kb = value;
         else if (k == "pdl") set_pdl(value != 0);
         else if (k == "coarse_mode") c->opt_coarse_mode = (int)value;
         else throw Fail{4, "set_option: unknown key " + k};
@@ -896,7 +1141,7 @@ int aspamg_gpu_upload_level(aspamg_gpu_ctx* c, int64_t level, const aspamg_csr_v
         GLevel l;
         l.n = (int)A->n_rows;
         l.a_nnz = A->nnz;
-        l.A = upload_mat(c, *A, true);
+        l.A = upload_mat(c, *A, true, 0);
         const bool has = G && G->n_rows > 0;
         if (has) {
             check_view(G, "G"); check_view(Gt, "Gt"); check_view(P, "P"); check_view(Pt, "Pt");
@@ -905,10 +1150,10 @@ int aspamg_gpu_upload_level(aspamg_gpu_ctx* c, int64_t level, const aspamg_csr_v
             if (P->n_rows != l.n || Pt->n_cols != l.n || Pt->n_rows != P->n_cols)
                 throw Fail{1, "upload_level: P must be n x n_c and P' n_c x n"};
             if (!(omega > 0.0) || !(omega <= 1.0)) throw Fail{4, "upload_level: omega must be in (0, 1]"};
-            l.G = upload_mat(c, *G, false);
-            l.Gt = upload_mat(c, *Gt, false);
-            l.P = upload_mat(c, *P, false);
-            l.Pt = upload_mat(c, *Pt, false);
+            l.G = upload_mat(c, *G, false, 1);
+            l.Gt = upload_mat(c, *Gt, false, 2);
+            l.P = upload_mat(c, *P, false, 3);
+            l.Pt = upload_mat(c, *Pt, false, 4);
             l.omega = omega;
             l.has_smoother = true;
         }
@@ -1024,8 +1269,8 @@ int aspamg_gpu_level_info(aspamg_gpu_ctx* c, int64_t level, aspamg_gpu_level_sta
         o->a_nnz = l.a_nnz;
         o->a_nnzb = l.A.fmt == 1 ? l.A.sb.nnzb : 0;
         o->a_fill = fill_ratio(l.A);
-        o->g_nnz = l.has_smoother ? (l.G.fmt == 2 ? l.G.sell.nnz : l.G.csr.nnz) : 0;
-        o->p_nnz = l.has_smoother ? (l.P.fmt == 2 ? l.P.sell.nnz : l.P.csr.nnz) : 0;
+        o->g_nnz = l.has_smoother ? l.G.nnz() : 0;
+        o->p_nnz = l.has_smoother ? l.P.nnz() : 0;
         o->omega = l.omega;
         o->alg_bytes_A = alg_bytes(l.A);
         if (l.has_smoother) {
@@ -1202,6 +1447,21 @@ int aspamg_gpu_pcg_device(aspamg_gpu_ctx* c, const double* b, const double* x0, 
     if (code != 0) return code;
     if (status == 6) c->err = "pcg: not converged";
     return status;
+}
+
+int aspamg_gpu_xsell_layout_spmv(const aspamg_csr_view* A, int64_t tile_rows, int64_t fold, int64_t gran, const double* x,
+                                 double* y) {
+    return guard(nullptr, [&] {
+        check_view(A, "A");
+        if (!x || !y) throw Fail{1, "xsell_layout_spmv: null vector"};
+        if (fold < 1 || fold > 2 || tile_rows < 32 * fold || tile_rows > kBlock * fold || tile_rows % (32 * fold) || gran < 1 ||
+            gran > 4)
+            throw Fail{4, "xsell_layout_spmv: tile_rows / fold must be a multiple of 32 in [32, 256], fold 1 or 2, gran in [1, 4]"};
+        XsellHost H;
+        if (!build_xsell_host(*A, (int)tile_rows, (int)fold, (int)gran, (size_t)65536, H))
+            throw Fail{4, "xsell_layout_spmv: operand does not fit the tile-local format"};
+        xsell_host_spmv(H, A->n_rows, A->n_cols, x, y);
+    });
 }
 
 int aspamg_gpu_last_solve_ms(aspamg_gpu_ctx* c, double* ms) {

@@ -69,6 +69,14 @@ struct aspamg_gpu_ctx {
     long long opt_sell_min_rows = 65536, opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
               opt_sell_u = 0, opt_sell_chh = 0, opt_sell_sort = 0,
               opt_sell_min_mean = 8;
+    // Tile-local SELL (kernels.cuh DXsell): bit mask over operand roles (1 A, 2 G, 4 G', 8 P, 16 P'),
+    // minimum rows, maximum mean row length, threads per CTA (0 = by size: 256 / 128 / 64), rows per
+    // lane (fold: 1, or 2 = long rows paired with short ones; a tile has threads x fold rows),
+    // footprint granule (log2 doubles), kernel variant (quads per group x 10 + min CTAs/SM),
+    // shared-memory budget per CTA.
+    long long opt_xsell = 30, opt_xsell_min_rows = 32768, opt_xsell_max_mean = 256, opt_xsell_rows = 0,
+              opt_xsell_rows256 = 400000, opt_xsell_rows128 = 100000, opt_xsell_gran = 3, opt_xsell_q = 0,
+              opt_xsell_smem_kb = 100, opt_xsell_fold = 2;
     // collapse the V-cycle below the first level with <= this many rows (0 = off);
     // C2 0.995 -> 0.966 ms/it, C1 0.120 -> 0.107 ms/it (profiles/tune_r01_tail_long.log)
     long long opt_tail_dense = 1500;
@@ -175,6 +183,8 @@ inline Red make_red(aspamg_gpu_ctx* c, int grid, int fin, double* out = nullptr)
 
 
 // Operand upload with per-operand format choice (sliced BSR3 / SELL / CSR).
-DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr);
+// role: 0 A, 1 G, 2 G', 3 P, 4 P' of a hierarchy level (eligible for the tile-local SELL format by
+// the "xsell" option mask), -1 anything else.
+DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr, int role = -1);
 
 }  // namespace aspamg_gpu

@@ -170,6 +170,16 @@ __device__ __forceinline__ unsigned short ld_keep(const unsigned short* p) {
     asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(r) : "l"(p), "l"(l2_keep_policy()));
     return r;
 }
+__device__ __forceinline__ double2 ld_keep(const double2* p) {
+    double2 r;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(l2_keep_policy()));
+    return r;
+}
+__device__ __forceinline__ uint2 ld_keep(const uint2* p) {
+    uint2 r;
+    asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(l2_keep_policy()));
+    return r;
+}
 template <int POL, class T>
 __device__ __forceinline__ T ld_mat(const T* p) {
     if constexpr (POL == 1) return __ldcs(p);
@@ -544,6 +554,154 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sell(DSell M, int epi, const d
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
 }
 
+// ------------------------------------------------------ tile-local SELL SpMV
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// One CTA per tile, F rows per lane (F = 1: sorted rank t; F = 2, "folded":
+// ranks t and R-1-t, a long row paired with a short one so the warps of a
+// tile carry nearly equal work). Phases: (1) cp.async the tile's x footprint
+// into shared memory; (2) meanwhile fetch the chunk metadata and the first
+// load group of the matrix stream (independent of x); (3) row sums over the
+// chunk's quads (row a's quads, then row b's), gathers from shared memory, the
+// next group's loads issued before the current group is consumed; (4) results
+// pass through shared memory back to natural row order, so the epilogue reads
+// aux / writes y coalesced.
+template <int Q, int STREAM, int MINB, int F>
+__global__ void __launch_bounds__(kBlock, MINB) k_xsell(DXsell M, int epi, const double* __restrict__ x, double* y,
+                                                       const double* aux, double omega, const double* dotw, Red red,
+                                                       const int* done) {
+    pdl_enter();
+    if (is_done(done)) return;
+    extern __shared__ __align__(16) double xsm[];
+    const int tid = threadIdx.x, lane = tid & 31, T = blockDim.x, R = F * T;
+    const int tile = blockIdx.x;
+    double* ys = xsm + M.fp_doubles;
+    const int2 tm = __ldg(M.tmeta + tile);
+    {
+        const int sh = M.gran - 1;  // 16-B pieces per granule = 1 << sh
+        const int np = tm.y << sh;
+        const int* lst = M.list + tm.x;
+        for (int p = tid; p < np; p += T) {
+            const int g = __ldg(lst + (p >> sh));
+            const int i0 = (g << M.gran) + 2 * (p & ((1 << sh) - 1));
+            if (i0 + 2 <= M.n_cols) {
+                cp_async16(xsm + 2 * p, x + i0);
+            } else {  // the last granule may straddle the end of x
+                xsm[2 * p] = i0 < M.n_cols ? x[i0] : 0.0;
+                xsm[2 * p + 1] = 0.0;
+            }
+        }
+        cp_async_commit();
+    }
+    const int r0 = tile * R;
+    const int lenA = M.len[r0 + tid];
+    const int prA = M.perm[r0 + tid];
+    const int lenB = F == 2 ? (int)M.len[r0 + R - 1 - tid] : 0;
+    const int prB = F == 2 ? (int)M.perm[r0 + R - 1 - tid] : 0;
+    const int2 cm = __ldg(M.cmeta + (tile * (T >> 5) + (tid >> 5)));
+    const bool need_aux = epi == EPI_RESID || epi == EPI_ADD || epi == EPI_ADDSCALE;
+    double av[F], dw[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+        const int orow = r0 + f * T + tid;  // this thread's output rows (natural order)
+        av[f] = (orow < M.n_rows && need_aux) ? aux[orow] : 0.0;
+        dw[f] = (orow < M.n_rows && dotw) ? dotw[orow] : 0.0;
+    }
+    const double2* vp = M.v + ((long long)cm.x * 64 + lane);
+    const uint2* cp = M.lc + ((long long)cm.x * 32 + lane);
+    const int qa = ((cm.y & 0xffff) + 3) >> 2;           // quads of the a rows (warp-uniform)
+    const int nq = qa + ((((unsigned)cm.y >> 16) + 3) >> 2);  // + quads of the b rows
+    auto rem_of = [&](int qi) { return qi < qa ? lenA - 4 * qi : lenB - 4 * (qi - qa); };
+    uint2 c[Q];
+    double2 v[Q][2];
+#pragma unroll
+    for (int u = 0; u < Q; ++u) {
+        const int rem = u < nq ? rem_of(u) : 0;
+        c[u] = rem > 0 ? ld_mat<STREAM>(cp + 32 * u) : make_uint2(0u, 0u);
+        v[u][0] = rem > 0 ? ld_mat<STREAM>(vp + 64 * u) : make_double2(0.0, 0.0);
+        v[u][1] = rem > 2 ? ld_mat<STREAM>(vp + 64 * u + 32) : make_double2(0.0, 0.0);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    double s = 0.0, sa = 0.0;
+    for (int q0 = 0; q0 < nq; q0 += Q) {
+        uint2 cc[Q];
+        double2 vv[Q][2];
+#pragma unroll
+        for (int u = 0; u < Q; ++u) {
+            cc[u] = c[u];
+            vv[u][0] = v[u][0];
+            vv[u][1] = v[u][1];
+        }
+        if (q0 + Q < nq) {
+#pragma unroll
+            for (int u = 0; u < Q; ++u) {
+                const int qq = q0 + Q + u;
+                const int rem = qq < nq ? rem_of(qq) : 0;
+                c[u] = rem > 0 ? ld_mat<STREAM>(cp + 32 * qq) : make_uint2(0u, 0u);
+                v[u][0] = rem > 0 ? ld_mat<STREAM>(vp + 64 * qq) : make_double2(0.0, 0.0);
+                v[u][1] = rem > 2 ? ld_mat<STREAM>(vp + 64 * qq + 32) : make_double2(0.0, 0.0);
+            }
+        }
+        double xv[Q][4];
+#pragma unroll
+        for (int u = 0; u < Q; ++u) {
+            xv[u][0] = xsm[cc[u].x & 0xffffu];
+            xv[u][1] = xsm[cc[u].x >> 16];
+            xv[u][2] = xsm[cc[u].y & 0xffffu];
+            xv[u][3] = xsm[cc[u].y >> 16];
+        }
+#pragma unroll
+        for (int u = 0; u < Q; ++u) {
+            const int qi = q0 + u;
+            if (F == 2 && qi == qa) {  // row a finished, row b starts (warp-uniform)
+                sa = s;
+                s = 0.0;
+            }
+            const int rem = qi < nq ? rem_of(qi) : 0;
+            if (rem > 0) s = __dadd_rn(s, __dmul_rn(vv[u][0].x, xv[u][0]));
+            if (rem > 1) s = __dadd_rn(s, __dmul_rn(vv[u][0].y, xv[u][1]));
+            if (rem > 2) s = __dadd_rn(s, __dmul_rn(vv[u][1].x, xv[u][2]));
+            if (rem > 3) s = __dadd_rn(s, __dmul_rn(vv[u][1].y, xv[u][3]));
+        }
+    }
+    if (F == 2) {
+        if (nq == qa) {  // no b quads: s still holds row a
+            sa = s;
+            s = 0.0;
+        }
+        ys[prA] = sa;
+        ys[prB] = s;
+    } else {
+        ys[prA] = s;
+    }
+    __syncthreads();
+    double dacc = 0.0;
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+        const int orow = r0 + f * T + tid;
+        if (orow < M.n_rows) {
+            const double r = ys[f * T + tid];
+            double out;
+            switch (epi) {
+                case EPI_SCALE: out = __dmul_rn(omega, r); break;
+                case EPI_RESID: out = __dsub_rn(av[f], r); break;
+                case EPI_ADD: out = __dadd_rn(av[f], r); break;
+                case EPI_ADDSCALE: out = __dadd_rn(av[f], __dmul_rn(omega, r)); break;
+                default: out = r;
+            }
+            y[orow] = out;
+            dacc = fma(out, dw[f], dacc);
+        }
+    }
+    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
+}
+
 // ------------------------------------------------------------- coarse tail
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
@@ -825,7 +983,26 @@ SpmvKern csr_kernel(const DCsr& A) {
     return A.ci16 ? csr_kernel_i<GG, P, true>(A) : csr_kernel_i<GG, P, false>(A);
 }
 #define CSRK(GG, P) csr_kernel<GG, P>(M.csr)
+using XsellKern = void (*)(DXsell, int, const double*, double*, const double*, double, const double*, Red, const int*);
+XsellKern xsell_kernel(const DXsell& X) {
+#define ASPAMG_XS(QQ, MB)                                                                              \
+    if (X.q == QQ * 10 + MB) {                                                                         \
+        if (X.fold == 2)                                                                               \
+            return X.pol == 1 ? k_xsell<QQ, 1, MB, 2> : X.pol == 2 ? k_xsell<QQ, 2, MB, 2> : k_xsell<QQ, 0, MB, 2>; \
+        return X.pol == 1 ? k_xsell<QQ, 1, MB, 1> : X.pol == 2 ? k_xsell<QQ, 2, MB, 1> : k_xsell<QQ, 0, MB, 1>;     \
+    }
+    ASPAMG_XS(1, 4)
+    ASPAMG_XS(1, 6)
+    ASPAMG_XS(2, 3)
+    ASPAMG_XS(2, 4)
+#undef ASPAMG_XS
+    if (X.fold == 2) return X.pol == 1 ? k_xsell<2, 1, 4, 2> : X.pol == 2 ? k_xsell<2, 2, 4, 2> : k_xsell<2, 0, 4, 2>;
+    return X.pol == 1 ? k_xsell<2, 1, 4, 1> : X.pol == 2 ? k_xsell<2, 2, 4, 1> : k_xsell<2, 0, 4, 1>;
+}
+size_t xsell_smem(const DXsell& X) { return sizeof(double) * ((size_t)X.fp_doubles + (size_t)X.R); }
+
 int spmv_grid(const DMat& M) {
+    if (M.fmt == 3) return M.xs.ntiles;
     if (M.fmt == 1) {
         const long long ch = (M.sb.nchunks + 7) / 8;
         return M.sb.pol == 1 ? occ_grid(k_sbsr3<1>, ch) : M.sb.pol == 2 ? occ_grid(k_sbsr3<2>, ch) : occ_grid(k_sbsr3<0>, ch);
@@ -869,6 +1046,11 @@ int spmv_grid(const DMat& M) {
 void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux, double omega, const double* dotw,
           const Red& red, const int* done, const Launch& L) {
     const int grid = L.grid > 0 ? L.grid : spmv_grid(M);
+    if (M.fmt == 3) {
+        launch(xsell_kernel(M.xs), M.xs.ntiles, M.xs.R / M.xs.fold, xsell_smem(M.xs), L.stream, M.xs, epi, x, y, aux, omega, dotw,
+               red, done);
+        return;
+    }
     if (M.fmt == 1) {
         if (M.sb.pol == 1)
             launch(k_sbsr3<1>, grid, kBlock, 0, L.stream, M.sb, epi, x, y, aux, omega, dotw, red, done);
@@ -967,6 +1149,19 @@ void tail_run(const TailOp* ops, int nops, GridBar* bar, const int* done, int gr
     cfg.attrs = attr;
     cfg.numAttrs = g_pdl ? 2 : 1;
     cudaLaunchKernelEx(&cfg, k_tail, ops, nops, bar, done);
+}
+
+// Opt in to the operand's dynamic shared memory on every variant that may run it.
+void xsell_prepare(const DXsell& X) {
+    const int need = (int)xsell_smem(X);
+    if (need <= 48 * 1024) return;
+    DXsell t = X;
+    for (int pol = 0; pol < 3; ++pol)
+        for (int q : {14, 16, 23, 24}) {
+            t.pol = pol;
+            t.q = q;
+            cudaFuncSetAttribute(xsell_kernel(t), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        }
 }
 
 void spmv_prepare() {

@@ -74,14 +74,51 @@ struct DSell {
     int* cb = nullptr;
 };
 
+// Tile-local SELL ("xsell"): rows in tiles of R rows (one CTA of R threads per
+// tile, one lane per row). Per tile the kernel first stages the tile's x
+// FOOTPRINT — the sorted list of the 2^gran-double granules of x its entries
+// reference — into shared memory with 16-B cp.async copies (each granule read
+// once per tile, fully coalesced), and the matrix stores 16-bit LOCAL columns
+// (granule rank << gran | offset) into that staged window. The x gathers of the
+// row sums then hit shared memory (bank conflicts only) instead of costing one
+// L1 wavefront per distinct line per warp instruction, which is what bounds
+// the lane-per-row kernels on scattered columns. Inside a tile the rows are
+// sorted by length (descending, stable) so each 32-row chunk is nearly
+// rectangular (with fold = 2 a lane owns two rows, rank t and rank R-1-t, whose
+// quads follow each other in the chunk); slots are stored in groups of four per lane ("quads": one 8-B
+// load of four 16-bit columns, two 16-B loads of values), chunk widths padded
+// to whole quads, padded entries predicated off. Local columns keep the
+// ascending global order, and every lane sums its row sequentially with
+// separate multiply / add: y is bit-identical to the reference spmv
+// (sparse_matrix.cpp:100-105).
+struct DXsell {
+    int n_rows = 0, n_cols = 0, ntiles = 0;
+    int R = 256;     // tile height (rows); the CTA has R / fold threads
+    int fold = 1;    // rows per lane: 1, or 2 = sorted rank t paired with rank R-1-t (balances the warps)
+    int gran = 3;    // log2 doubles per footprint granule
+    long long nnz = 0, quads = 0, list_len = 0;
+    int2* tmeta = nullptr;           // per tile {list offset, granule count}
+    int2* cmeta = nullptr;           // per chunk {quad offset, width of the a rows | width of the b rows << 16}
+    unsigned short* len = nullptr;   // per slot row (sorted order), padded to ntiles * R
+    unsigned short* perm = nullptr;  // per slot row: local row inside the tile
+    int* list = nullptr;             // footprint granule ids, tile after tile
+    double2* v = nullptr;            // quad q of a chunk, half h, lane l at v[((off + q) * 2 + h) * 32 + l]
+    uint2* lc = nullptr;             // quad q, lane l at lc[(off + q) * 32 + l]: four 16-bit local columns
+    int fp_doubles = 0;              // staged window capacity (largest tile footprint), in doubles
+    int pol = 0;
+    int q = 2;                       // quads per load group (kernel variant)
+};
+
 // One matrix operand.
 struct DMat {
-    int fmt = 0;  // 0 CSR (group per row), 1 sliced BSR3, 2 SELL-32
+    int fmt = 0;  // 0 CSR (group per row), 1 sliced BSR3, 2 SELL-32, 3 tile-local SELL
     DCsr csr;
     DSbsr3 sb;
     DSell sell;
-    int rows() const { return fmt == 1 ? 3 * sb.nb : fmt == 2 ? sell.n_rows : csr.n_rows; }
-    int cols() const { return fmt == 1 ? 3 * sb.nbc : fmt == 2 ? sell.n_cols : csr.n_cols; }
+    DXsell xs;
+    int rows() const { return fmt == 1 ? 3 * sb.nb : fmt == 2 ? sell.n_rows : fmt == 3 ? xs.n_rows : csr.n_rows; }
+    int cols() const { return fmt == 1 ? 3 * sb.nbc : fmt == 2 ? sell.n_cols : fmt == 3 ? xs.n_cols : csr.n_cols; }
+    long long nnz() const { return fmt == 1 ? 9 * sb.nnzb : fmt == 2 ? sell.nnz : fmt == 3 ? xs.nnz : csr.nnz; }
 };
 
 // Epilogue of y = f(M x):
@@ -177,6 +214,7 @@ int tail_grid();
 
 void set_pdl(bool on);          // programmatic dependent launch on/off (process-wide)
 void spmv_prepare();          // once per process, outside any stream capture
+void xsell_prepare(const DXsell& M);  // once per operand, outside any stream capture (dynamic smem opt-in)
 void coarse_prepare(int n);  // once per factor size, outside any stream capture
 void fill_zero(int n, double* y, const int* done, const Launch& L);
 

@@ -61,7 +61,7 @@ def test_spmv_every_operand_every_level(c1_ctx, pkg, which):
         x = rng.standard_normal(m.n_cols)
         yg = g.spmv(l, wi, x)
         yo = o.spmv(l, which, x)
-        if g.level_info(l).fmt[wi] in (1, 2):  # sliced formats: reference order, bit-exact
+        if g.level_info(l).fmt[wi] in (1, 2, 3):  # sliced formats: reference order, bit-exact
             assert np.array_equal(yg, yo), (which, l)
             continue
         # per-entry bound: |sum| error <= nnz_row * eps * sum|a_ij x_j|
@@ -280,14 +280,14 @@ def test_sell_layout_variants_are_bit_identical(pkg, opts):
     column order, so the V-cycle output is bit-identical across variants."""
     p, h = problem_and_hierarchy(2, 2)
     y = np.random.default_rng(5).standard_normal(p.K.n_rows)
-    ref = _gpu(pkg, h, sell_chh=32, sell_sort_fill_pct=100000, sell_min_mean=1).apply(y)
-    opts = dict(opts, sell_min_mean=1)
+    ref = _gpu(pkg, h, sell_chh=32, sell_sort_fill_pct=100000, sell_min_mean=1, xsell=0).apply(y)
+    opts = dict(opts, sell_min_mean=1, xsell=0)
     if "sell_sort" not in opts:  # keep every SELL-eligible operand in SELL (CSR trees differ in bits)
         opts.setdefault("sell_sort_fill_pct", 100000)
     g = _gpu(pkg, h, **opts)
     assert np.array_equal(g.apply(y), ref)
     if "pdl" in opts:
-        g2 = _gpu(pkg, h, pdl=1, sell_chh=32, sell_sort_fill_pct=100000, sell_min_mean=1)  # restore the default
+        g2 = _gpu(pkg, h, pdl=1, sell_chh=32, sell_sort_fill_pct=100000, sell_min_mean=1, xsell=0)  # restore the default
         assert np.array_equal(g2.apply(y), ref)
 
 
@@ -297,9 +297,9 @@ def test_csr_kernel_variants_are_bit_identical(pkg, opts):
     thread's entries and their order, so the V-cycle output is bit-identical."""
     p, h = problem_and_hierarchy(2, 2)
     y = np.random.default_rng(9).standard_normal(p.K.n_rows)
-    base = {"idx16": 0} if opts.get("idx16") == 0 else {}
+    base = {"idx16": 0, "xsell": 0} if opts.get("idx16") == 0 else {"xsell": 0}
     ref = _gpu(pkg, h, csr_pf=1, **base).apply(y)
-    assert np.array_equal(_gpu(pkg, h, **opts).apply(y), ref)
+    assert np.array_equal(_gpu(pkg, h, xsell=0, **opts).apply(y), ref)
 
 
 @pytest.mark.parametrize("opts", [{"csr_long": 1}, {"csr_long": 2}, {"csr_long": 4, "csr_pf": 0},
@@ -309,7 +309,7 @@ def test_csr_long_row_split_matches_oracle(pkg, oracle, opts):
     CTAs of the same launch): every operand within the CSR per-row bound, PCG
     within the north_star tolerances, deterministic run to run."""
     p, h = problem_and_hierarchy(2, 2)
-    g = _gpu(pkg, h, **opts)
+    g = _gpu(pkg, h, xsell=0, **opts)
     o = _oracle(oracle, h)
     rng = np.random.default_rng(13)
     for l in range(h.n_levels - 1):
@@ -337,6 +337,43 @@ def test_dense_coarse_tail_matches_oracle(pkg, oracle, rows):
     y = np.random.default_rng(17).standard_normal(p.K.n_rows)
     assert rel_err(g.apply(y), o.vcycle(y)) < RTOL_VCYCLE
     assert np.array_equal(g.apply(y), g.apply(y))
+    _pcg_parity(p, h, g, o)
+
+
+@pytest.mark.parametrize("opts", [{}, {"xsell_rows": 256}, {"xsell_rows": 128, "xsell_gran": 4}, {"xsell_rows": 64, "xsell_gran": 2},
+                                  {"xsell_rows": 32, "xsell_gran": 1}, {"xsell_q": 14}, {"xsell_q": 16}, {"xsell_q": 23},
+                                  {"xsell_fold": 1}, {"xsell_fold": 1, "xsell_rows": 256, "xsell_q": 23},
+                                  {"xsell_fold": 1, "xsell_q": 14, "xsell_gran": 4}, {"xsell_fold": 1, "xsell_q": 16},
+                                  {"xsell": 31, "xsell_max_mean": 100000, "xsell_rows": 64}, {"xsell_smem_kb": 8}])
+def test_xsell_operands_bit_exact_and_pcg_parity(pkg, oracle, opts):
+    """Tile-local SELL (x footprint staged in shared memory, 16-bit local columns):
+    every operand uploaded in that format multiplies bit-identically to the
+    oracle spmv (sequential ascending sums, sparse_matrix.cpp:100-105) for every
+    tile height / granule / kernel variant; operands that do not fit the
+    shared-memory budget fall back to SELL / CSR; V-cycle and PCG parity hold."""
+    p, h = problem_and_hierarchy(2, 2)
+    g = _gpu(pkg, h, xsell_min_rows=0, **opts)
+    o = _oracle(oracle, h)
+    rng = np.random.default_rng(29)
+    n3 = 0
+    for l in range(h.n_levels - 1):
+        for wi, which in enumerate(["A", "G", "Gt", "P", "Pt"]):
+            m = getattr(h.level(l, copy=False), which)
+            x = rng.standard_normal(m.n_cols)
+            yg, yo = g.spmv(l, wi, x), o.spmv(l, which, x)
+            if g.level_info(l).fmt[wi] == 3:
+                n3 += 1
+                assert np.array_equal(yg, yo), (opts, which, l)
+            else:
+                absrow = np.abs(m.to_scipy()) @ np.abs(x)
+                assert np.all(np.abs(yg - yo) <= 1e-14 * absrow + 1e-300), (opts, which, l)
+    assert n3 >= (4 if opts.get("xsell_smem_kb") != 8 else 0), n3
+    y = rng.standard_normal(p.K.n_rows)
+    assert np.array_equal(g.apply(y), g.apply(y))
+    assert rel_err(g.apply(y), o.vcycle(y)) < RTOL_VCYCLE
+    # smoothing step and epilogues (resid / add / addscale) through the xsell operands
+    b = rng.standard_normal(p.K.n_rows)
+    assert rel_err(g.smooth(0, b, y), o.smooth(0, b, y)) < 1e-12
     _pcg_parity(p, h, g, o)
 
 
@@ -372,7 +409,7 @@ def test_sell_all_empty_row_groups(pkg):
     ctx = C.c_void_p()
     assert lib.aspamg_gpu_ctx_create(0, C.byref(ctx)) == 0
     try:
-        for k, v in {"sell_min_rows": 0, "sell_min_mean": 0, "sell_chh": 32, "bsr": 0, "tail_dense": 0}.items():
+        for k, v in {"sell_min_rows": 0, "sell_min_mean": 0, "sell_chh": 32, "bsr": 0, "tail_dense": 0, "xsell": 0}.items():
             assert lib.aspamg_gpu_set_option(ctx, k.encode(), v) == 0
         for l, ms in enumerate((mats0, mats1)):
             views = [m.view() for m in ms]

@@ -21,7 +21,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def raw_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Raw page of a report: a .ncu-rep (read through ncu) or an already exported raw CSV."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     return r[0], r[2:]
 
@@ -60,6 +64,10 @@ def main():
     ap.add_argument("--regex", default="k_sell|k_csr|k_sbsr3")
     ap.add_argument("--skip", type=int, default=0, help="-s used for the capture (filtered launches skipped)")
     ap.add_argument("--traffic-key", default="c2")
+    ap.add_argument("--all-ops", action="store_true",
+                    help="the capture holds every launch of one iteration in op order (tools/run_profile.sh)")
+    ap.add_argument("--peak", type=float, default=6550.4, help="measured HBM copy peak, GB/s (MEASURED_PEAKS.json)")
+    ap.add_argument("--build-tag", default=None, help="kernel build hash for traffic.json (bench.kernel_build_tag())")
     args = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
@@ -75,6 +83,8 @@ def main():
         rx = re.compile(args.regex)
         filt = [o for o in body if rx.search(kernel_of(o[0]) or "-")]
         seq = (filt * 3)[args.skip % max(len(filt), 1):]
+        if args.all_ops:
+            seq = body
         out = []
         traffic = {}
         for k, row in enumerate(rows):
@@ -91,6 +101,11 @@ def main():
                    "regs": g(row, "launch__registers_per_thread"),
                    "warps_active": g(row, "sm__warps_active.avg.per_cycle_active"),
                    "l2_hit_pct": g(row, "lts__t_sector_hit_rate.pct"),
+                   "dram_over_alg": (rd + wr) * 1e6 / op[3] if op[3] else 0.0,
+                   "frac_of_peak": (op[3] / 1e6 / dur * 1e3 / args.peak) if dur else 0.0,
+                   "dram_pct": g(row, "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+                   "l1tex_pct": g(row, "l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                   "lts_pct": g(row, "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
                    "top_stalls": "; ".join(f"{n}={v:.1f}" for v, n in stalls)}
             out.append(rec)
             traffic[f"{op[0]}@L{op[1]}"] = (rd + wr) * 1e6
@@ -102,7 +117,10 @@ def main():
         print("wrote", path)
         tpath = os.path.join(prof, "traffic.json")
         tj = json.load(open(tpath)) if os.path.exists(tpath) else {}
-        tj.setdefault(args.traffic_key, {}).update(traffic)
+        if args.build_tag:
+            tj.setdefault(args.build_tag, {}).setdefault(args.traffic_key, {}).update(traffic)
+        else:
+            tj.setdefault(args.traffic_key, {}).update(traffic)
         json.dump(tj, open(tpath, "w"), indent=1)
         print("updated", tpath)
     if args.launches:

@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--scale", type=int, default=1)
+    ap.add_argument("--gpu-setup", type=int, default=1, help="SRQCG / aFSAI / Galerkin on the GPU (the identical hierarchy)")
     ap.add_argument("--opt", nargs="*", default=[])
     args = ap.parse_args()
 
@@ -27,7 +28,8 @@ def main():
         def barrier(self):
             pass
 
-    prob, h, _, _, _ = bench.get_hierarchy(P, args.config, args.scale, 0, D(), os.cpu_count() or 1)
+    prob, h, _, _, _ = bench.get_hierarchy(P, args.config, args.scale, 0, D(), os.cpu_count() or 1,
+                                            0 if args.gpu_setup else None)
     opts = {k: int(v) for k, v in (o.split("=") for o in args.opt)}
     g = P.GpuVcycle(h, device=0, options=opts)
     # ncu runs this with --profile-from-start off: only the two body runs below are

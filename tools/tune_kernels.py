@@ -31,6 +31,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--scale", type=int, default=1)
+    ap.add_argument("--gpu-setup", type=int, default=1, help="SRQCG / aFSAI / Galerkin on the GPU (the identical hierarchy)")
     ap.add_argument("--sets", nargs="*", default=None)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "tune.json"))
     args = ap.parse_args()
@@ -45,7 +46,8 @@ def main():
         def barrier(self):
             pass
 
-    prob, h, _, _, _ = bench.get_hierarchy(P, args.config, args.scale, 0, D(), os.cpu_count() or 1)
+    prob, h, _, _, _ = bench.get_hierarchy(P, args.config, args.scale, 0, D(), os.cpu_count() or 1,
+                                            0 if args.gpu_setup else None)
     res = {}
     for name, opts in sets.items():
         g = P.GpuVcycle(h, device=0, options=opts)
