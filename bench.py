@@ -8,7 +8,9 @@ by the setup and uploaded once. ``value`` is seconds per PCG iteration over the
 timed solves (inputs resident in HBM); ``ms_per_step`` and ``time_to_1e8_s``
 are the time-to-1e-8 of one solve. ``e2e`` is the same metric through the
 C-ABI call with host buffers (H2D of b, D2H of x and the residual history
-inside the timed region).
+inside the timed region): ONE loop of aspamg_gpu_pcg calls on pinned host
+buffers yields both — wall clock around the call (e2e) and the CUDA-event time
+of the solve alone, recorded after b is resident in HBM (value).
 
 ``--impl reference`` times the reference's CPU path on the host cores: the
 restated pcg / vcycle_apply (oracle/oracle.c) driving the reference's own
@@ -240,10 +242,24 @@ def run_reference(args, ws, rank):
             pass
 
     threads = os.cpu_count() or 1
-    # the hierarchy is the solve's INPUT (north_star: produced by the CPU setup);
-    # only the solve below is timed
-    prob, h, t_gen, t_setup, origin = get_hierarchy(P, args.config, args.scale, 0, _D(), threads)
-    oh, use_ref, iters = cpu_reference_sample(h, prob.rhs, threads, target_s=args.ref_sample_s)
+    # The hierarchy is the solve's INPUT (north_star: produced once by the setup); only
+    # the CPU solve below is timed. When a GPU is visible the setup's SRQCG / aFSAI /
+    # Galerkin phases run on it (bit-identical hierarchy, tests/test_gpu_setup.py; C5:
+    # 278 s instead of 688 s on 16 cores) so that a cold box reaches the timed CPU
+    # solve sooner; --cpu-setup keeps the setup on the host.
+    setup_device = None
+    if not args.cpu_setup:
+        try:
+            from paper_1902_01715_b200 import _native as N
+            nd = C.c_int(0)
+            if N.gpu().aspamg_gpu_device_count(C.byref(nd)) == 0 and nd.value > 0:
+                setup_device = 0
+        except Exception:
+            setup_device = None
+    prob, h, t_gen, t_setup, origin = get_hierarchy(P, args.config, args.scale, 0, _D(), threads, setup_device)
+    # bounded sample per step: the whole run (warmup + steps) stays near ref_total_s
+    per_step_s = min(args.ref_sample_s, args.ref_total_s / max(1, args.warmup + args.steps))
+    oh, use_ref, iters = cpu_reference_sample(h, prob.rhs, threads, target_s=per_step_s)
     times, its = [], 0
     for step in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -300,82 +316,67 @@ def run_b200(args, ws, rank, local):
     lib = N.gpu()
     n = prob.K.n_rows
     nbytes = 8 * n
-    # device-resident inputs for the kernel-level value
-    b_dev = C.c_void_p()
-    x_dev = C.c_void_p()
-    g._chk(lib.aspamg_gpu_alloc_device(g._ctx, nbytes, C.byref(b_dev)))
-    g._chk(lib.aspamg_gpu_alloc_device(g._ctx, nbytes, C.byref(x_dev)))
     rhs = np.ascontiguousarray(prob.rhs)
-    g._chk(lib.aspamg_gpu_memcpy(g._ctx, b_dev, rhs.ctypes.data_as(C.c_void_p), nbytes))
     max_it = args.max_it
-    hist = np.empty(max_it)
     n_it = C.c_int64()
     conv = C.c_int()
     trr = C.c_double()
     Pd = C.POINTER(C.c_double)
-
-    def solve_dev():
-        code = lib.aspamg_gpu_pcg_device(g._ctx, b_dev, None, args.tol, max_it, x_dev, hist.ctypes.data_as(Pd),
-                                         C.byref(n_it), C.byref(conv), C.byref(trr))
-        if code not in (0, 6):
-            g._chk(code)
-        ms = C.c_double()
-        lib.aspamg_gpu_last_solve_ms(g._ctx, C.byref(ms))
-        lc = C.c_int64()
-        lib.aspamg_gpu_launch_count(g._ctx, C.byref(lc))
-        return ms.value, int(n_it.value), bool(conv.value), float(trr.value), int(lc.value)
-
-    for _ in range(args.warmup):
-        solve_dev()
-    dist.barrier()
-    clk = ClockSampler(local)
-    clk.start()
-    tot_ms, tot_it, launches = 0.0, 0, 0
-    per_solve = []
-    for _ in range(args.steps):
-        ms, it, cv, tr, lc = solve_dev()
-        tot_ms += ms
-        tot_it += it
-        launches += lc
-        per_solve.append((ms, it, cv, tr))
-    clocks = clk.stop()
-    dist.barrier()
-    # whole job: slowest rank's device time over the PCG iterations of ALL ranks
-    # (replicas: every rank solves its own copy; N ranks do N x the iterations)
-    # replicas: value = the slowest rank's seconds per PCG iteration (each rank runs the
-    # same solve); the job's aggregate throughput is reported separately
-    tot_ms = dist.max(tot_ms)
-    job_it = dist.sum(float(tot_it))
-    value = (tot_ms / 1e3) / max(tot_it, 1)
-    job_its_per_s = job_it / (tot_ms / 1e3) if tot_ms > 0 else None
-    n_iters = per_solve[-1][1]
-    converged = all(p[2] for p in per_solve)
-
-    # e2e through the public C-ABI with pinned host buffers (H2D b, D2H x + history)
+    # ONE timed loop gives both numbers. Each step is the public C-ABI call
+    # aspamg_gpu_pcg on pinned HOST buffers: H2D of b, the solve, D2H of x and the
+    # residual history. e2e = wall clock around the call. value = the device time
+    # of the solve alone (CUDA events on the context stream, recorded after the H2D
+    # copy of b has been enqueued, i.e. inputs resident in HBM; run_pcg, context.cu).
     pin_b = C.c_void_p()
     pin_x = C.c_void_p()
     pin_h = C.c_void_p()
     lib.aspamg_gpu_alloc_pinned(nbytes, C.byref(pin_b))
     lib.aspamg_gpu_alloc_pinned(nbytes, C.byref(pin_x))
-    lib.aspamg_gpu_alloc_pinned(8 * max_it, C.byref(pin_h))
+    lib.aspamg_gpu_alloc_pinned(8 * (max_it + 1), C.byref(pin_h))
     C.memmove(pin_b, rhs.ctypes.data, nbytes)
-    e2e_t, e2e_it = 0.0, 0
     bp = C.cast(pin_b, Pd)
     xp = C.cast(pin_x, Pd)
     hp = C.cast(pin_h, Pd)
-    for s in range(args.warmup + args.steps):
+
+    def solve_host():
         t0 = time.perf_counter()
         code = lib.aspamg_gpu_pcg(g._ctx, bp, None, args.tol, max_it, xp, hp, C.byref(n_it), C.byref(conv),
                                   C.byref(trr))
         dt = time.perf_counter() - t0
         if code not in (0, 6):
             g._chk(code)
-        if s >= args.warmup:
-            e2e_t += dt
-            e2e_it += int(n_it.value)
+        ms = C.c_double()
+        lib.aspamg_gpu_last_solve_ms(g._ctx, C.byref(ms))
+        lc = C.c_int64()
+        lib.aspamg_gpu_launch_count(g._ctx, C.byref(lc))
+        return ms.value, int(n_it.value), bool(conv.value), float(trr.value), int(lc.value), dt
+
+    for _ in range(args.warmup):
+        solve_host()
+    dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    tot_ms, tot_it, launches, e2e_t = 0.0, 0, 0, 0.0
+    per_solve = []
+    for _ in range(args.steps):
+        ms, it, cv, tr, lc, dt = solve_host()
+        tot_ms += ms
+        tot_it += it
+        launches += lc
+        e2e_t += dt
+        per_solve.append((ms, it, cv, tr))
+    clocks = clk.stop()
+    dist.barrier()
+    # replicas: value = the slowest rank's seconds per PCG iteration (each rank runs the
+    # same solve); the job's aggregate throughput is reported separately
+    tot_ms = dist.max(tot_ms)
     e2e_t = dist.max(e2e_t)
-    e2e_value = e2e_t / max(e2e_it, 1)
-    x_host = np.ctypeslib.as_array(xp, shape=(n,)).copy()
+    job_it = dist.sum(float(tot_it))
+    value = (tot_ms / 1e3) / max(tot_it, 1)
+    e2e_value = e2e_t / max(tot_it, 1)
+    job_its_per_s = job_it / (tot_ms / 1e3) if tot_ms > 0 else None
+    n_iters = per_solve[-1][1]
+    converged = all(p[2] for p in per_solve)
     lib.aspamg_gpu_free_pinned(pin_b)
     lib.aspamg_gpu_free_pinned(pin_x)
     lib.aspamg_gpu_free_pinned(pin_h)
@@ -461,6 +462,7 @@ def run_b200(args, ws, rank, local):
         "job_iterations_per_s": job_its_per_s,
         "clocks": clocks,
         "time_to_1e8_s": tot_ms / args.steps / 1e3,
+        "e2e_time_to_1e8_s": e2e_t / args.steps,
     }
     if cpu:
         line["cpu_baseline"] = cpu
@@ -480,6 +482,8 @@ def main():
     ap.add_argument("--max-it", dest="max_it", type=int, default=1000)
     ap.add_argument("--kernel-reps", dest="kernel_reps", type=int, default=20)
     ap.add_argument("--ref-sample-s", dest="ref_sample_s", type=float, default=12.0)
+    ap.add_argument("--ref-total-s", dest="ref_total_s", type=float, default=150.0,
+                    help="reference arm: CPU seconds over all warmup + timed steps (each step samples PCG iterations)")
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
     ap.add_argument("--no-cpu-1t", dest="no_cpu_1t", action="store_true")
     ap.add_argument("--cpu-setup", dest="cpu_setup", action="store_true",
