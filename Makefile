@@ -31,9 +31,16 @@ $(LIB)/obj/smalldense.o: $(PKG)/csrc/host/smalldense.cpp $(PKG)/csrc/host/smalld
 	@mkdir -p $(LIB)/obj
 	$(CXX) $(CXXFLAGS) -fvisibility=hidden -c -o $@ $<
 
-$(LIB)/libaspamg_gpu.so: $(GPUSRC) $(GPUHDR) $(HOSTHDR) $(LIB)/obj/smalldense.o
+# The device assembler shares the element-stiffness source with the host
+# (host/hex_stiffness.hpp): -fmad=false is the device side of the host's
+# -ffp-contract=off, so both round every product and sum separately.
+$(LIB)/obj/assemble_gpu.o: $(PKG)/csrc/gpu/assemble_gpu.cu $(GPUHDR) $(HOSTHDR)
+	@mkdir -p $(LIB)/obj
+	$(NVCC) $(NVFLAGS) -fmad=false -c -o $@ $< 2> $(LIB)/ptxas_assemble.log || (cat $(LIB)/ptxas_assemble.log; exit 1)
+
+$(LIB)/libaspamg_gpu.so: $(GPUSRC) $(GPUHDR) $(HOSTHDR) $(LIB)/obj/smalldense.o $(LIB)/obj/assemble_gpu.o
 	@mkdir -p $(LIB)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(GPUSRC) $(LIB)/obj/smalldense.o -lgomp 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(filter-out %/assemble_gpu.cu,$(GPUSRC)) $(LIB)/obj/smalldense.o $(LIB)/obj/assemble_gpu.o -lgomp 2> $(LIB)/ptxas.log || (cat $(LIB)/ptxas.log; exit 1)
 
 # C++ `solve` CLI on the C++ host API (include/aspamg_b200.hpp); finds the two
 # libraries next to itself (rpath $$ORIGIN).

@@ -36,4 +36,21 @@ typedef struct aspamg_smoother_params {
     uint64_t seed;
 } aspamg_smoother_params;
 
+/* Mesh description handed to an assembly backend (aspamg_set_assembly_backend,
+ * aspamg_host.h; aspamg_gpu_assemble_hex, aspamg_gpu.h). */
+typedef struct aspamg_hex_assembly {
+    int64_t nx, ny, nz;        /* elements per axis; nodes are (nx+1)(ny+1)(nz+1), node = i + (nx+1)(j + (ny+1)k) */
+    int64_t n_free;            /* free (unclamped) nodes; K is 3 n_free x 3 n_free, dofs interleaved */
+    int32_t cube;              /* 1: undistorted cubes of spacing h, one stiffness per table entry (fem.cpp:153-158);
+                                  0: one stiffness per element from its 8 node coordinates */
+    double h;
+    const double* node_xyz;    /* all nodes, row-major x y z */
+    const int64_t* free_index; /* node -> free node id, or -1 (clamped) */
+    const int64_t* free_node;  /* free node id -> node */
+    const int32_t* el_ke;      /* element (ex + nx (ey + ny ez)) -> stiffness-table entry */
+    int64_t n_ke;              /* stiffness-table entries (distinct materials, or elements) */
+    const double* young;       /* per table entry */
+    const double* poisson;
+} aspamg_hex_assembly;
+
 #endif

@@ -145,6 +145,14 @@ int aspamg_gpu_set_setup_policy(const char* key, double value);
 int aspamg_gpu_afsai_build(void* device, const aspamg_csr_view* A, int64_t k, int64_t rho, double eps,
                            aspamg_csr_alloc_fn alloc, void* sink, double* psi);
 
+/* GPU setup: assembly of the structured-hex elasticity stiffness
+ * (fem.cpp:87-184: 2x2x2-Gauss element stiffness, pattern, element-order fill) on the
+ * device, bit-identical to the host generator's K (same element-stiffness source, no FMA
+ * contraction, every entry summed in element order). K is written through alloc(sink, ...)
+ * as the reference-layout CSR. Signature = aspamg_assembly_fn of aspamg_host.h.
+ * device = (void*)(intptr_t)index. Status 3: inverted / degenerate element. */
+int aspamg_gpu_assemble_hex(void* device, const aspamg_hex_assembly* in, aspamg_csr_alloc_fn alloc, void* sink);
+
 /* Layout self-check of the tile-local SELL format ("xsell") — host only, no
  * device needed: builds the format's arrays for A exactly as upload does and walks them on
  * the CPU with the kernel's indexing (staged x window, 16-bit local columns, quads, tile

@@ -110,6 +110,14 @@ int aspamg_set_galerkin_backend(aspamg_galerkin_fn fn, void* user);
  * is owned by *out (free with aspamg_csr_free). */
 int aspamg_galerkin(const aspamg_csr_view* P, const aspamg_csr_view* A, aspamg_csr_owned** out,
                     aspamg_csr_view* out_view);
+/* Assembly backend (fem.cpp:87-184): when set, the generator
+ * (aspamg_problem_config / aspamg_problem_hex) hands the element stiffness matrices, the
+ * CSR pattern and the fill of K to fn (e.g. aspamg_gpu_assemble_hex), which writes K
+ * through alloc(sink, ...). The mesh description is computed on the host (node
+ * coordinates incl. the seeded perturbation, clamp -> free numbering, material table).
+ * fn must reproduce the host assembly bit for bit. NULL restores the CPU path. */
+typedef int (*aspamg_assembly_fn)(void* user, const aspamg_hex_assembly* in, aspamg_csr_alloc_fn alloc, void* sink);
+int aspamg_set_assembly_backend(aspamg_assembly_fn fn, void* user);
 /* Smoother backend: when set, aspamg_setup runs each level's
  * adaptive FSAI set-up through fn (e.g. aspamg_gpu_smoother_setup); the host forms the
  * Kaporin estimate from the returned psi. fn may return -1 to decline a level (the

@@ -115,6 +115,7 @@ def host() -> C.CDLL:
         lib.aspamg_set_srqcg_backend.argtypes = [C.c_void_p, C.c_void_p]
         lib.aspamg_set_galerkin_backend.argtypes = [C.c_void_p, C.c_void_p]
         lib.aspamg_set_smoother_backend.argtypes = [C.c_void_p, C.c_void_p]
+        lib.aspamg_set_assembly_backend.argtypes = [C.c_void_p, C.c_void_p]
         lib.aspamg_galerkin.argtypes = [C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(C.c_void_p),
                                         C.POINTER(CsrView)]
         _host = lib
@@ -166,6 +167,7 @@ def gpu() -> C.CDLL:
         lib.aspamg_gpu_srqcg.argtypes = [vp, C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(CsrView), P_dbl, i64, i64,
                                          i64, dbl, C.c_uint64, P_dbl, P_dbl, P_i64, P_i64, C.POINTER(C.c_int)]
         lib.aspamg_gpu_galerkin.argtypes = [vp, C.POINTER(CsrView), C.POINTER(CsrView), C.POINTER(CsrView), vp, vp]
+        lib.aspamg_gpu_assemble_hex.argtypes = [vp, vp, vp, vp]
         lib.aspamg_gpu_set_setup_policy.argtypes = [C.c_char_p, dbl]
         lib.aspamg_gpu_afsai_build.argtypes = [vp, C.POINTER(CsrView), i64, i64, dbl, vp, vp, P_dbl]
         lib.aspamg_gpu_smoother_setup.argtypes = [vp, C.POINTER(CsrView), C.POINTER(SmootherParams), vp, vp, P_dbl,

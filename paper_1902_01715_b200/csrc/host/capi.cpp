@@ -361,6 +361,38 @@ int aspamg_set_galerkin_backend(aspamg_galerkin_fn fn, void* user) {
     return 0;
 }
 
+// ------------------------------------------------------ external assembly backend
+namespace {
+aspamg_assembly_fn g_assembly_fn = nullptr;
+void* g_assembly_user = nullptr;
+}  // namespace
+
+namespace aspamg {
+
+bool assembly_backend_set() { return g_assembly_fn != nullptr; }
+
+void assemble_external(const aspamg_hex_assembly& in, Csr& K) {
+    const index_t n = K.n_rows;
+    const bool sym = K.symmetric;
+    const int st = g_assembly_fn(g_assembly_user, &in, csr_sink_alloc, &K);
+    if (st != 0) {
+        const std::string msg = "assembly backend failed with status " + std::to_string(st);
+        if (st == 3) throw NumericalError("assembly: inverted or degenerate element");
+        if (st == 4) throw ConfigError(msg);
+        throw std::runtime_error(msg);
+    }
+    if (K.n_rows != n || K.n_cols != n) throw DimensionError("assembly backend returned a matrix of the wrong size");
+    K.symmetric = sym;
+}
+
+}  // namespace aspamg
+
+int aspamg_set_assembly_backend(aspamg_assembly_fn fn, void* user) {
+    g_assembly_fn = fn;
+    g_assembly_user = user;
+    return 0;
+}
+
 int aspamg_galerkin(const aspamg_csr_view* P, const aspamg_csr_view* A, aspamg_csr_owned** out,
                     aspamg_csr_view* out_view) {
     return guard([&] {

@@ -1,5 +1,6 @@
 // Structured hex elasticity generator; see fem.hpp for the reference mapping.
 #include "fem.hpp"
+#include "hex_stiffness.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -16,135 +17,19 @@ void Material::validate() const {
         throw ConfigError("material: Poisson ratio must lie in (-1, 0.5)");
 }
 
-namespace {
-
-// fem.cpp:18-28 (isotropic D in Voigt order xx,yy,zz,xy,yz,zx)
-void elastic_matrix(const Material& m, double D[6][6]) {
-    const double E = m.young_modulus, nu = m.poisson_ratio;
-    const double lambda = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
-    const double mu = E / (2.0 * (1.0 + nu));
-    for (int i = 0; i < 6; ++i)
-        for (int j = 0; j < 6; ++j) D[i][j] = 0.0;
-    D[0][0] = D[1][1] = D[2][2] = lambda + 2.0 * mu;
-    D[0][1] = D[0][2] = D[1][0] = D[1][2] = D[2][0] = D[2][1] = lambda;
-    D[3][3] = D[4][4] = D[5][5] = mu;
-}
-
-// fem.cpp:30-34: local node a = ia + 2 ja + 4 ka
-constexpr double kSign[8][3] = {{-1, -1, -1}, {1, -1, -1}, {-1, 1, -1}, {1, 1, -1},
-                                {-1, -1, 1},  {1, -1, 1},  {-1, 1, 1},  {1, 1, 1}};
-
-// Accumulate det * B' D B for one Gauss point given physical gradients.
-void add_btdb(const double grad[8][3], const double D[6][6], double det, double K[24][24]) {
-    double B[6][24];
-    for (int r = 0; r < 6; ++r)
-        for (int c = 0; c < 24; ++c) B[r][c] = 0.0;
-    for (int a = 0; a < 8; ++a) {  // fem.cpp:67-78
-        const double dx = grad[a][0], dy = grad[a][1], dz = grad[a][2];
-        B[0][3 * a + 0] = dx;
-        B[1][3 * a + 1] = dy;
-        B[2][3 * a + 2] = dz;
-        B[3][3 * a + 0] = dy;
-        B[3][3 * a + 1] = dx;
-        B[4][3 * a + 1] = dz;
-        B[4][3 * a + 2] = dy;
-        B[5][3 * a + 0] = dz;
-        B[5][3 * a + 2] = dx;
-    }
-    double BtD[24][6];
-    for (int i = 0; i < 24; ++i)
-        for (int k = 0; k < 6; ++k) {
-            double s = 0.0;
-            for (int l = 0; l < 6; ++l) s += B[l][i] * D[l][k];
-            BtD[i][k] = s;
-        }
-    for (int i = 0; i < 24; ++i)
-        for (int j = 0; j < 24; ++j) {
-            double s = 0.0;
-            for (int k = 0; k < 6; ++k) s += BtD[i][k] * B[k][j];
-            K[i][j] += det * s;
-        }
-}
-
-void mirror_lower(double K[24][24]) {  // fem.cpp:81-83
-    for (int i = 0; i < 24; ++i)
-        for (int j = 0; j < i; ++j) K[j][i] = K[i][j];
-}
-
-}  // namespace
-
-// fem.cpp:37-85 (regular grid: constant Jacobian 2/h, det h^3/8)
+// fem.cpp:37-85 (regular grid: constant Jacobian 2/h, det h^3/8); the arithmetic
+// lives in hex_stiffness.hpp, shared with the device assembler.
 void hex_element_stiffness_cube(double h, const Material& m, double Ke[24][24]) {
     m.validate();
     if (!(h > 0.0)) throw ConfigError("assembly: spacing must be positive");
-    double D[6][6];
-    elastic_matrix(m, D);
-    const double gp = 1.0 / std::sqrt(3.0);
-    const double det_j = h * h * h / 8.0;
-    for (int i = 0; i < 24; ++i)
-        for (int j = 0; j < 24; ++j) Ke[i][j] = 0.0;
-    double grad[8][3];
-    for (int gx = 0; gx < 2; ++gx)
-        for (int gy = 0; gy < 2; ++gy)
-            for (int gz = 0; gz < 2; ++gz) {
-                const double xi = gp * (2 * gx - 1), eta = gp * (2 * gy - 1), zeta = gp * (2 * gz - 1);
-                const double scale = 2.0 / h;
-                for (int a = 0; a < 8; ++a) {
-                    const double sx = kSign[a][0], sy = kSign[a][1], sz = kSign[a][2];
-                    grad[a][0] = 0.125 * sx * (1.0 + sy * eta) * (1.0 + sz * zeta) * scale;
-                    grad[a][1] = 0.125 * sy * (1.0 + sx * xi) * (1.0 + sz * zeta) * scale;
-                    grad[a][2] = 0.125 * sz * (1.0 + sx * xi) * (1.0 + sy * eta) * scale;
-                }
-                add_btdb(grad, D, det_j, Ke);
-            }
-    mirror_lower(Ke);
+    hexk::stiffness_cube(h, m.young_modulus, m.poisson_ratio, 1.0 / std::sqrt(3.0), &Ke[0][0]);
 }
 
 // General isoparametric trilinear hex (extension for distorted meshes, C3).
 void hex_element_stiffness(const double xyz[8][3], const Material& m, double Ke[24][24]) {
     m.validate();
-    double D[6][6];
-    elastic_matrix(m, D);
-    const double gp = 1.0 / std::sqrt(3.0);
-    for (int i = 0; i < 24; ++i)
-        for (int j = 0; j < 24; ++j) Ke[i][j] = 0.0;
-    for (int gx = 0; gx < 2; ++gx)
-        for (int gy = 0; gy < 2; ++gy)
-            for (int gz = 0; gz < 2; ++gz) {
-                const double xi = gp * (2 * gx - 1), eta = gp * (2 * gy - 1), zeta = gp * (2 * gz - 1);
-                double dn[8][3];
-                for (int a = 0; a < 8; ++a) {
-                    const double sx = kSign[a][0], sy = kSign[a][1], sz = kSign[a][2];
-                    dn[a][0] = 0.125 * sx * (1.0 + sy * eta) * (1.0 + sz * zeta);
-                    dn[a][1] = 0.125 * sy * (1.0 + sx * xi) * (1.0 + sz * zeta);
-                    dn[a][2] = 0.125 * sz * (1.0 + sx * xi) * (1.0 + sy * eta);
-                }
-                double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // J[i][j] = dx_j/dxi_i
-                for (int a = 0; a < 8; ++a)
-                    for (int i = 0; i < 3; ++i)
-                        for (int j = 0; j < 3; ++j) J[i][j] += dn[a][i] * xyz[a][j];
-                const double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
-                                   J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
-                                   J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
-                if (!(det > 0.0)) throw NumericalError("assembly: inverted or degenerate element");
-                double Ji[3][3];
-                Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / det;
-                Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
-                Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
-                Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / det;
-                Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
-                Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
-                Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / det;
-                Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
-                Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
-                // grad_x N = J^{-1} grad_xi N
-                double grad[8][3];
-                for (int a = 0; a < 8; ++a)
-                    for (int i = 0; i < 3; ++i)
-                        grad[a][i] = Ji[i][0] * dn[a][0] + Ji[i][1] * dn[a][1] + Ji[i][2] * dn[a][2];
-                add_btdb(grad, D, det, Ke);
-            }
-    mirror_lower(Ke);
+    if (!hexk::stiffness_general(xyz, m.young_modulus, m.poisson_ratio, 1.0 / std::sqrt(3.0), &Ke[0][0]))
+        throw NumericalError("assembly: inverted or degenerate element");
 }
 
 GeneratedProblem assemble_hex(const MeshSpec& mesh, const std::vector<Material>& materials) {
@@ -212,7 +97,7 @@ GeneratedProblem assemble_hex(const MeshSpec& mesh, const std::vector<Material>&
     // on distorted / anisotropic meshes.
     const bool cube = mesh.perturb == 0.0 && mesh.hx == mesh.hy && mesh.hy == mesh.hz;
     std::vector<int> el_ke(static_cast<size_t>(n_el));
-    std::vector<std::array<double, 576>> ke_table;
+    std::vector<double> ke_young, ke_poisson;  // material of each stiffness-table entry
     if (cube) {
         std::map<std::pair<double, double>, int> seen;
         for (index_t e = 0; e < n_el; ++e) {
@@ -220,15 +105,50 @@ GeneratedProblem assemble_hex(const MeshSpec& mesh, const std::vector<Material>&
                                             materials[static_cast<size_t>(e)].poisson_ratio);
             auto it = seen.find(key);
             if (it == seen.end()) {
-                it = seen.emplace(key, static_cast<int>(ke_table.size())).first;
-                ke_table.emplace_back();
-                hex_element_stiffness_cube(mesh.hx, materials[static_cast<size_t>(e)],
-                                           reinterpret_cast<double(*)[24]>(ke_table.back().data()));
+                it = seen.emplace(key, static_cast<int>(ke_young.size())).first;
+                ke_young.push_back(key.first);
+                ke_poisson.push_back(key.second);
             }
             el_ke[static_cast<size_t>(e)] = it->second;
         }
     } else {
-        ke_table.resize(static_cast<size_t>(n_el));
+        ke_young.resize(static_cast<size_t>(n_el));
+        ke_poisson.resize(static_cast<size_t>(n_el));
+        for (index_t e = 0; e < n_el; ++e) {
+            ke_young[static_cast<size_t>(e)] = materials[static_cast<size_t>(e)].young_modulus;
+            ke_poisson[static_cast<size_t>(e)] = materials[static_cast<size_t>(e)].poisson_ratio;
+            el_ke[static_cast<size_t>(e)] = static_cast<int>(e);
+        }
+    }
+    Csr& K = P.stiffness;
+    K.n_rows = K.n_cols = 3 * n_free;
+    K.symmetric = true;
+
+    // Assembly backend: element stiffness, pattern and fill on
+    // the device (aspamg_gpu_assemble_hex), bit-identical to the host path below.
+    if (assembly_backend_set()) {
+        aspamg_hex_assembly in{};
+        in.nx = nx; in.ny = ny; in.nz = nz;
+        in.n_free = n_free;
+        in.cube = cube ? 1 : 0;
+        in.h = mesh.hx;
+        in.node_xyz = P.node_xyz.data();
+        in.free_index = P.free_index.data();
+        in.free_node = free_node.data();
+        in.el_ke = el_ke.data();
+        in.n_ke = static_cast<int64_t>(ke_young.size());
+        in.young = ke_young.data();
+        in.poisson = ke_poisson.data();
+        assemble_external(in, K);
+        return P;
+    }
+
+    std::vector<std::array<double, 576>> ke_table(ke_young.size());
+    if (cube) {
+        for (size_t q = 0; q < ke_table.size(); ++q)
+            hex_element_stiffness_cube(mesh.hx, Material{ke_young[q], ke_poisson[q]},
+                                       reinterpret_cast<double(*)[24]>(ke_table[q].data()));
+    } else {
 #pragma omp parallel for schedule(static) num_threads(num_threads())
         for (index_t e = 0; e < n_el; ++e) {
             const index_t ex = e % nx, ey = (e / nx) % ny, ez = e / (nx * ny);
@@ -239,15 +159,11 @@ GeneratedProblem assemble_hex(const MeshSpec& mesh, const std::vector<Material>&
             }
             hex_element_stiffness(xyz, materials[static_cast<size_t>(e)],
                                   reinterpret_cast<double(*)[24]>(ke_table[static_cast<size_t>(e)].data()));
-            el_ke[static_cast<size_t>(e)] = static_cast<int>(e);
         }
     }
 
     // CSR pattern: row node f couples with every free node in its 3x3x3
     // neighbourhood; neighbours ascend in node id == ascending free id.
-    Csr& K = P.stiffness;
-    K.n_rows = K.n_cols = 3 * n_free;
-    K.symmetric = true;
     std::vector<index_t> deg(static_cast<size_t>(n_free));
 #pragma omp parallel for schedule(static) num_threads(num_threads())
     for (index_t f = 0; f < n_free; ++f) {

@@ -14,6 +14,7 @@
 #pragma once
 
 #include "core.hpp"
+#include "../../../include/aspamg_host.h"
 
 #include <array>
 #include <vector>
@@ -54,6 +55,11 @@ struct GeneratedProblem {
 void hex_element_stiffness(const double xyz[8][3], const Material& m, double Ke[24][24]);
 // The reference's regular-cube path (fem.cpp:37-85), spacing h on all axes.
 void hex_element_stiffness_cube(double h, const Material& m, double Ke[24][24]);
+
+// Assembly backend (capi.cpp, aspamg_set_assembly_backend): when set, assemble_hex
+// hands the element stiffness + pattern + fill to it (the device assembler).
+bool assembly_backend_set();
+void assemble_external(const aspamg_hex_assembly& in, Csr& K);
 
 GeneratedProblem assemble_hex(const MeshSpec& mesh, const std::vector<Material>& materials);
 

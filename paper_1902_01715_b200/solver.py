@@ -151,17 +151,41 @@ class Problem:
         _chk_host(lib.aspamg_problem_coords(self._h, C.byref(rp), C.byref(n)))
         self.coords = _borrow(rp, (n.value, 3), self) if n.value else np.zeros((0, 3))
 
+    @staticmethod
+    def _assembly_backend(device: Optional[int]):
+        """Route the stiffness assembly (element matrices, pattern, fill) to the GPU
+        assembler on that device; K is bit-identical."""
+        lib = N.host()
+        if device is None:
+            lib.aspamg_set_assembly_backend(None, None)
+        else:
+            lib.aspamg_set_assembly_backend(C.cast(N.gpu().aspamg_gpu_assemble_hex, C.c_void_p),
+                                            C.c_void_p(int(device)) if device else None)
+
     @classmethod
-    def config(cls, cfg: int, scale: int = 1) -> "Problem":
+    def config(cls, cfg: int, scale: int = 1, assembly_device: Optional[int] = None) -> "Problem":
         h = C.c_void_p()
-        _chk_host(N.host().aspamg_problem_config(cfg, scale, C.byref(h)))
+        if assembly_device is not None:
+            cls._assembly_backend(assembly_device)
+        try:
+            _chk_host(N.host().aspamg_problem_config(cfg, scale, C.byref(h)))
+        finally:
+            if assembly_device is not None:
+                cls._assembly_backend(None)
         return cls(h)
 
     @classmethod
     def hex_cube(cls, nx: int, ny: Optional[int] = None, nz: Optional[int] = None, spacing: float = 1.0,
-                 young: float = 1.0, poisson: float = 0.3, clamp: int = 16) -> "Problem":
+                 young: float = 1.0, poisson: float = 0.3, clamp: int = 16,
+                 assembly_device: Optional[int] = None) -> "Problem":
         h = C.c_void_p()
-        _chk_host(N.host().aspamg_problem_hex(nx, ny or nx, nz or nx, spacing, young, poisson, clamp, C.byref(h)))
+        if assembly_device is not None:
+            cls._assembly_backend(assembly_device)
+        try:
+            _chk_host(N.host().aspamg_problem_hex(nx, ny or nx, nz or nx, spacing, young, poisson, clamp, C.byref(h)))
+        finally:
+            if assembly_device is not None:
+                cls._assembly_backend(None)
         return cls(h)
 
     def __del__(self):
@@ -264,6 +288,23 @@ class Hierarchy:
         f = lambda v: SparseMatrix.from_view(v, copy, None if copy else self)  # noqa: E731
         return LevelData(f(lv.A), f(lv.G), f(lv.Gt), f(lv.P), f(lv.Pt), lv.omega, lv.lambda_hat,
                          int(lv.refinement_passes), int(lv.smoother_exit), int(lv.n_tv), float(lv.t_smoother))
+
+    def signature(self, stride: int = 1009) -> str:
+        """Content hash of the hierarchy (sizes, nnz, omega and every stride-th value /
+        column of each operand, the coarse factor): golden fixtures recorded on one
+        hierarchy (tests/golden) are only compared against the same hierarchy."""
+        import hashlib
+        hh = hashlib.sha1()
+        for l in range(self.n_levels):
+            d = self.level(l, copy=False)
+            hh.update(np.float64(d.omega).tobytes())
+            for m in (d.A, d.G, d.Gt, d.P, d.Pt):
+                hh.update(np.array([m.n_rows, m.n_cols, m.nnz], dtype=np.int64).tobytes())
+                if m.nnz:
+                    hh.update(np.ascontiguousarray(m.values[::stride]).tobytes())
+                    hh.update(np.ascontiguousarray(m.col_indices[::stride]).tobytes())
+        hh.update(np.ascontiguousarray(self.coarse_factor().ravel()[::7]).tobytes())
+        return hh.hexdigest()
 
     def coarse_factor(self) -> np.ndarray:
         n = C.c_int64()

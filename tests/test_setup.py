@@ -164,6 +164,11 @@ def test_setup_deterministic_across_thread_counts(pkg):
             assert np.array_equal(getattr(a, name).values, getattr(b, name).values)
             assert np.array_equal(getattr(a, name).col_indices, getattr(b, name).col_indices)
     assert np.array_equal(h1.coarse_factor(), h4.coarse_factor())
+    # the content signature golden fixtures are keyed on (tests/golden/c5_oracle.npz)
+    assert h1.signature() == h4.signature()
+    q = pkg.Problem.config(1, 5)
+    assert pkg.Hierarchy.setup(q.K, q.coords).signature() != h1.signature()
+    assert h1.signature(stride=7) != h1.signature(stride=11)
 
 
 def test_hierarchy_save_load_roundtrip(pkg, tmp_path):
