@@ -393,12 +393,15 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr, int
         len[(size_t)i] = (int)(v.row_offsets[i + 1] - v.row_offsets[i]);
         maxlen = std::max(maxlen, len[(size_t)i]);
     }
-    if (role >= 0 && ((c->opt_xsell >> role) & 1) && v.n_rows >= c->opt_xsell_min_rows &&
+    // "fuse_rr": the restriction runs inside the residual kernel (k_resid_restrict / k_tail),
+    // which walks plain CSR rows — P' then skips the sliced formats and the long-row split
+    const bool plain_csr = role == 4 && c->opt_fuse_rr;
+    if (!plain_csr && role >= 0 && ((c->opt_xsell >> role) & 1) && v.n_rows >= c->opt_xsell_min_rows &&
         mean <= (double)c->opt_xsell_max_mean && build_xsell(c, v, M.xs)) {
         M.fmt = 3;
         return M;
     }
-    bool sell = v.n_rows >= c->opt_sell_min_rows && mean <= (double)c->opt_sell_max_mean &&
+    bool sell = !plain_csr && v.n_rows >= c->opt_sell_min_rows && mean <= (double)c->opt_sell_max_mean &&
                 mean >= (double)c->opt_sell_min_mean && maxlen <= c->opt_sell_max_len;
     if (sell && c->opt_sell_chh == 0 && !c->opt_sell_sort && nnz > 0) {
         // natural order only (sorted SELL loses the x-gather locality): fall back
@@ -504,7 +507,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr, int
     A.nnz = nnz;
     A.group = group_for(mean, maxlen, v.n_rows, (double)c->opt_csr_per_thread);
     A.pf = (int)c->opt_csr_pf;
-    if (c->opt_csr_long > 0 && A.group <= 16) {
+    if (c->opt_csr_long > 0 && A.group <= 16 && !plain_csr) {
         const int thr = (int)c->opt_csr_long * A.group * 4;
         std::vector<int> lr;
         for (int64_t i = 0; i < v.n_rows; ++i)
@@ -663,6 +666,54 @@ bool build_tail(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* y,
     return true;
 }
 
+// "fuse_rr": r = y - A s and r_c = P' r of level k as ONE cooperative launch (grid
+// barrier between the two phases, r read back through L2). Level 0 with the sliced
+// BSR3 K uses k_resid_restrict; levels whose A and P' are both plain CSR use the
+// op-table kernel with two ops. Returns false when the level's formats do not fit.
+bool add_resid_restrict(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* s, const double* y, double* yc,
+                        const int* done) {
+    GLevel& l = c->lv[(size_t)k];
+    if (l.Pt.fmt != 0 || l.Pt.csr.nlong) return false;
+    TailOp pt{};
+    pt.kind = 0;
+    pt.epi = EPI_PLAIN;
+    pt.M = l.Pt.csr;
+    pt.x = l.r;
+    pt.y = yc;
+    pt.omega = 1.0;
+    pt.n = l.Pt.rows();
+    const double bytes = alg_bytes(l.A) + 8.0 * l.n + alg_bytes(l.Pt);
+    double* r = l.r;
+    if (l.A.fmt == 1) {
+        GridBar* bar = dalloc<GridBar>(c, 1);
+        CK(cudaMemset(bar, 0, sizeof(GridBar)));
+        const DSbsr3 A = l.A.sb;
+        const int grid = resid_restrict_grid(A.pol);
+        ops.push_back({"resid_restrict.sbsr3+" + fmt_name(l.Pt), k, bytes,
+                       [=](cudaStream_t st) { resid_restrict(A, pt, s, r, y, bar, done, grid, st); }});
+        return true;
+    }
+    if (l.A.fmt != 0 || l.A.csr.nlong) return false;
+    TailOp d[2] = {};
+    d[0].kind = 0;
+    d[0].epi = EPI_RESID;
+    d[0].M = l.A.csr;
+    d[0].x = s;
+    d[0].y = r;
+    d[0].aux = y;
+    d[0].omega = 1.0;
+    d[0].n = l.n;
+    d[1] = pt;
+    TailOp* dd = dalloc<TailOp>(c, 2);
+    CK(cudaMemcpy(dd, d, sizeof(d), cudaMemcpyHostToDevice));
+    GridBar* bar = dalloc<GridBar>(c, 1);
+    CK(cudaMemset(bar, 0, sizeof(GridBar)));
+    const int grid = tail_grid();
+    ops.push_back({"resid_restrict." + fmt_name(l.A) + "+" + fmt_name(l.Pt), k, bytes,
+                   [=](cudaStream_t st) { tail_run(dd, 2, bar, done, grid, st); }});
+    return true;
+}
+
 void build_vcycle(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* y, double* z, const double* dotw0,
                   int fin0, const int* done, bool allow_tail) {
     const int L = (int)c->lv.size();
@@ -717,8 +768,10 @@ void build_vcycle(aspamg_gpu_ctx* c, std::vector<Op>& ops, int k, const double* 
         ops.back().desc.n = n;
     }
     // r = y - A s ; r_c = P' r
-    add_spmv(c, ops, "resid_A", k, l.A, EPI_RESID, s, l.r, y, 1.0, nullptr, FIN_NONE, nullptr, done);
-    add_spmv(c, ops, "restrict_Pt", k, l.Pt, EPI_PLAIN, l.r, yc, nullptr, 1.0, nullptr, FIN_NONE, nullptr, done);
+    if (!(c->opt_fuse_rr && add_resid_restrict(c, ops, k, s, y, yc, done))) {
+        add_spmv(c, ops, "resid_A", k, l.A, EPI_RESID, s, l.r, y, 1.0, nullptr, FIN_NONE, nullptr, done);
+        add_spmv(c, ops, "restrict_Pt", k, l.Pt, EPI_PLAIN, l.r, yc, nullptr, 1.0, nullptr, FIN_NONE, nullptr, done);
+    }
     build_vcycle(c, ops, k + 1, yc, zc, dotw0, fin0, done, allow_tail);
     // s += P e_c
     const bool last_is_prolong = c->nu2 == 0;
@@ -1106,6 +1159,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "xsell_gran") c->opt_xsell_gran = value;
         else if (k == "xsell_q") c->opt_xsell_q = value;
         else if (k == "xsell_smem_kb") c->opt_xsell_smem_kb = value;
+        else if (k == "fuse_rr") c->opt_fuse_rr = value;
         else if (k == "pdl") set_pdl(value != 0);
         else if (k == "coarse_mode") c->opt_coarse_mode = (int)value;
         else throw Fail{4, "set_option: unknown key " + k};

@@ -69,17 +69,20 @@ struct aspamg_gpu_ctx {
     long long opt_sell_min_rows = 65536, opt_sell_max_mean = 48, opt_sell_max_len = 64, opt_sell_sigma = 4096, opt_sell_sort_fill_pct = 110,
               opt_sell_u = 0, opt_sell_chh = 0, opt_sell_sort = 0,
               opt_sell_min_mean = 8;
-    // Tile-local SELL (kernels.cuh DXsell): bit mask over operand roles (1 A, 2 G, 4 G', 8 P, 16 P'),
+    // Tile-local SELL (kernels.cuh DXsell), OFF by default: measured slower than SELL / CSR on every
+    // operand role except the level-0 G' (C2: 37-45 vs 40-48 us; G 36 vs 31, P' 34 vs 12 us;
+    // profiles/tune_r02_c2_xsell.json). Bit mask over operand roles (1 A, 2 G, 4 G', 8 P, 16 P'),
     // minimum rows, maximum mean row length, threads per CTA (0 = by size: 256 / 128 / 64), rows per
     // lane (fold: 1, or 2 = long rows paired with short ones; a tile has threads x fold rows),
     // footprint granule (log2 doubles), kernel variant (quads per group x 10 + min CTAs/SM),
     // shared-memory budget per CTA.
-    long long opt_xsell = 30, opt_xsell_min_rows = 32768, opt_xsell_max_mean = 256, opt_xsell_rows = 0,
+    long long opt_xsell = 0, opt_xsell_min_rows = 32768, opt_xsell_max_mean = 256, opt_xsell_rows = 0,
               opt_xsell_rows256 = 400000, opt_xsell_rows128 = 100000, opt_xsell_gran = 3, opt_xsell_q = 0,
               opt_xsell_smem_kb = 100, opt_xsell_fold = 2;
     // collapse the V-cycle below the first level with <= this many rows (0 = off);
     // C2 0.995 -> 0.966 ms/it, C1 0.120 -> 0.107 ms/it (profiles/tune_r01_tail_long.log)
     long long opt_tail_dense = 1500;
+    long long opt_fuse_rr = 0;  // restriction fused with the residual (one cooperative launch per level)
     long long opt_csr_long = 4;  // long-row split threshold in rounds (rows > long*T*4 entries; 0 = off)
     long long opt_csr_pf = 1;  // CSR (T <= 16): prefetch the next row's pointers (measured 1.4% faster per PCG iteration on C2)
     long long opt_idx16 = 1;  // 16-bit column offsets where every row spans < 2^16 columns

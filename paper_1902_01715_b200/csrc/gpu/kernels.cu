@@ -348,16 +348,13 @@ constexpr int SB_U = 3;    // block slots per load group (sliced BSR3)
 // row sums run sequentially in ascending column order with separate multiply
 // and add — exactly the reference spmv's arithmetic (sparse_matrix.cpp:100-105),
 // so y is bit-identical to it.
+// The chunk loop of the sliced BSR3 product for warp `warp` of `nwarps`; the dot
+// contribution of the rows it writes is added to dacc.
 template <int STREAM>
-__global__ void __launch_bounds__(kBlock) k_sbsr3(DSbsr3 M, int epi, const double* __restrict__ x, double* y,
-                                                   const double* aux, double omega, const double* dotw, Red red,
-                                                   const int* done) {
-    pdl_enter();
-    if (is_done(done)) return;
+__device__ __forceinline__ void sbsr3_rows(const DSbsr3& M, int epi, const double* __restrict__ x, double* y,
+                                           const double* aux, double omega, const double* dotw, int warp,
+                                           int nwarps, double& dacc) {
     const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * kBlock) >> 5;
-    double dacc = 0.0;
     for (int ch = warp; ch < M.nchunks; ch += nwarps) {
         const int br = ch * 32 + lane;
         const bool act = br < M.nb;
@@ -425,6 +422,17 @@ __global__ void __launch_bounds__(kBlock) k_sbsr3(DSbsr3 M, int epi, const doubl
             }
         }
     }
+}
+
+template <int STREAM>
+__global__ void __launch_bounds__(kBlock) k_sbsr3(DSbsr3 M, int epi, const double* __restrict__ x, double* y,
+                                                   const double* aux, double omega, const double* dotw, Red red,
+                                                   const int* done) {
+    pdl_enter();
+    if (is_done(done)) return;
+    double dacc = 0.0;
+    sbsr3_rows<STREAM>(M, epi, x, y, aux, omega, dotw, (blockIdx.x * kBlock + threadIdx.x) >> 5,
+                       (gridDim.x * kBlock) >> 5, dacc);
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
 }
 
@@ -659,7 +667,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_xsell(DXsell M, int epi, const
 #pragma unroll
         for (int u = 0; u < Q; ++u) {
             const int qi = q0 + u;
-            if (F == 2 && qi == qa) {  // row a finished, row b starts (warp-uniform)
+            // row a finished, row b starts (warp-uniform). Only when b quads exist: a group's
+            // trailing slot qi == nq == qa must not clear the finished sum (handled after the loop).
+            if (F == 2 && qi == qa && qa < nq) {
                 sa = s;
                 s = 0.0;
             }
@@ -800,6 +810,25 @@ __global__ void __launch_bounds__(kBlock) k_tail(const TailOp* __restrict__ ops,
         }
         if (i + 1 < nops) grid_barrier(bar);
     }
+}
+
+// Restriction fused with the fine residual (Alg. 2):
+// ONE cooperative launch computes r = y - A s with the sliced BSR3 chunk loop, crosses
+// a grid barrier, and gathers r_c = P' r (CSR rows, T threads each) while r is still
+// L2-resident. Same per-row arithmetic and trees as the two separate kernels, so the
+// results are bit-identical to the unfused path; no atomics on the data.
+template <int STREAM>
+__global__ void __launch_bounds__(kBlock) k_resid_restrict(DSbsr3 A, TailOp pt, const double* __restrict__ s,
+                                                            double* r, const double* y, GridBar* bar,
+                                                            const int* done) {
+    pdl_enter();
+    if (is_done(done)) return;
+    __shared__ double wsum[kBlock / 32];
+    double dacc = 0.0;
+    sbsr3_rows<STREAM>(A, EPI_RESID, s, r, y, 1.0, nullptr, (blockIdx.x * kBlock + threadIdx.x) >> 5,
+                       (gridDim.x * kBlock) >> 5, dacc);
+    grid_barrier(bar);
+    tail_csr(pt, wsum);
 }
 
 // ------------------------------------------------------------- PCG vectors
@@ -975,6 +1004,8 @@ template <int GG, int P, bool I16>
 SpmvKern csr_kernel_i(const DCsr& A) {
     if constexpr (GG <= 16) {
         if (A.pf) return k_csr<GG, P, I16, 4, true>;
+    } else if constexpr (GG <= 64 && !I16) {
+        if (A.pf >= 2) return k_csr<GG, P, I16, 4, true>;  // opt-in: prefetch for warp-per-row operands too
     }
     return k_csr<GG, P, I16, 4>;
 }
@@ -1149,6 +1180,33 @@ void tail_run(const TailOp* ops, int nops, GridBar* bar, const int* done, int gr
     cfg.attrs = attr;
     cfg.numAttrs = g_pdl ? 2 : 1;
     cudaLaunchKernelEx(&cfg, k_tail, ops, nops, bar, done);
+}
+
+int resid_restrict_grid(int pol) {
+    int per_sm = 0;
+    if (pol == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resid_restrict<1>, kBlock, 0);
+    else if (pol == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resid_restrict<2>, kBlock, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resid_restrict<0>, kBlock, 0);
+    if (per_sm <= 0) per_sm = 1;
+    return num_sms() * per_sm;
+}
+
+void resid_restrict(const DSbsr3& A, const TailOp& pt, const double* s, double* r, const double* y, GridBar* bar,
+                    const int* done, int grid, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)kBlock);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the software grid barrier
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl ? 2 : 1;
+    if (A.pol == 1) cudaLaunchKernelEx(&cfg, k_resid_restrict<1>, A, pt, s, r, y, bar, done);
+    else if (A.pol == 2) cudaLaunchKernelEx(&cfg, k_resid_restrict<2>, A, pt, s, r, y, bar, done);
+    else cudaLaunchKernelEx(&cfg, k_resid_restrict<0>, A, pt, s, r, y, bar, done);
 }
 
 // Opt in to the operand's dynamic shared memory on every variant that may run it.

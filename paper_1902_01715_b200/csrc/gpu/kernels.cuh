@@ -211,6 +211,11 @@ struct GridBar {
 };
 void tail_run(const TailOp* ops, int nops, GridBar* bar, const int* done, int grid, cudaStream_t s);
 int tail_grid();
+// r = y - A s (sliced BSR3) and r_c = P' r (pt: a CSR product op, x = r) in one
+// cooperative launch with a grid barrier in between (option "fuse_rr").
+void resid_restrict(const DSbsr3& A, const TailOp& pt, const double* s, double* r, const double* y, GridBar* bar,
+                    const int* done, int grid, cudaStream_t st);
+int resid_restrict_grid(int pol);
 
 void set_pdl(bool on);          // programmatic dependent launch on/off (process-wide)
 void spmv_prepare();          // once per process, outside any stream capture

@@ -325,6 +325,35 @@ def test_csr_long_row_split_matches_oracle(pkg, oracle, opts):
     _pcg_parity(p, h, g, o)
 
 
+@pytest.mark.parametrize("cfg,scale,opts", [(2, 2, {}), (2, 2, {"bsr": 0}), (1, 1, {"tail_dense": 0}), (3, 4, {})])
+def test_fused_residual_restriction_matches_oracle(pkg, oracle, cfg, scale, opts):
+    """Restriction fused with the fine residual (fuse_rr):
+    one cooperative launch per level computes r = y - A s, crosses a grid barrier and
+    gathers r_c = P' r. Level 0 runs the sliced-BSR3 variant (k_resid_restrict), CSR
+    levels the two-op table kernel. V-cycle within 1e-11 of the oracle and within
+    rounding of the unfused path, deterministic, PCG inside the north_star gates."""
+    p, h = problem_and_hierarchy(cfg, scale)
+    g = _gpu(pkg, h, fuse_rr=1, **opts)
+    g0 = _gpu(pkg, h, fuse_rr=0, **opts)
+    o = _oracle(oracle, h)
+    names = [(n, l) for n, l, _, _ in g.profile_iteration()]
+    fused = [(n, l) for n, l in names if n.startswith("resid_restrict")]
+    assert fused and (fused[0][1] == 0), names
+    if "bsr" not in opts:
+        assert fused[0][0].startswith("resid_restrict.sbsr3+csr")
+    assert not any(n.startswith("restrict_Pt") and l == 0 for n, l in names)
+    rng = np.random.default_rng(29)
+    for _ in range(2):
+        y = rng.standard_normal(p.K.n_rows)
+        zf = g.apply(y)
+        assert np.array_equal(zf, g.apply(y))
+        assert rel_err(zf, o.vcycle(y)) < RTOL_VCYCLE
+        assert rel_err(zf, g0.apply(y)) < 1e-13
+    _pcg_parity(p, h, g, o)
+    g.close()
+    g0.close()
+
+
 @pytest.mark.parametrize("rows", [0, 300, 2000, 8000])
 def test_dense_coarse_tail_matches_oracle(pkg, oracle, rows):
     """Collapsed coarse tail (tail_dense): the V-cycle below the first level
@@ -352,7 +381,7 @@ def test_xsell_operands_bit_exact_and_pcg_parity(pkg, oracle, opts):
     tile height / granule / kernel variant; operands that do not fit the
     shared-memory budget fall back to SELL / CSR; V-cycle and PCG parity hold."""
     p, h = problem_and_hierarchy(2, 2)
-    g = _gpu(pkg, h, xsell_min_rows=0, **opts)
+    g = _gpu(pkg, h, xsell_min_rows=0, **{"xsell": 30, **opts})  # the format is opt-in (default mask 0)
     o = _oracle(oracle, h)
     rng = np.random.default_rng(29)
     n3 = 0

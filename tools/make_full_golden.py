@@ -34,12 +34,22 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--max-it", type=int, default=1000)
     ap.add_argument("--gpu-setup", type=int, default=1)
+    ap.add_argument("--cached", type=int, default=1)
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     out = args.out or os.path.join(ROOT, "gpurun_out", f"c{args.config}_oracle.npz")
     t0 = time.perf_counter()
-    p = P.Problem.config(args.config, 1)
-    h = P.Hierarchy.setup(p.K, p.coords, setup_device=0 if args.gpu_setup else None)
+    if args.cached:  # reuse bench.py's hierarchy cache (.cache/): a save/load round trip is bit-exact
+        import bench
+
+        class _D:
+            def barrier(self):
+                pass
+        p, h, _, _, _ = bench.get_hierarchy(P, args.config, 1, 0, _D(), os.cpu_count() or 1,
+                                            0 if args.gpu_setup else None)
+    else:
+        p = P.Problem.config(args.config, 1)
+        h = P.Hierarchy.setup(p.K, p.coords, setup_device=0 if args.gpu_setup else None)
     t_setup = time.perf_counter() - t0
     sig = h.signature()
     print("setup", round(t_setup, 1), "s, signature", sig, flush=True)

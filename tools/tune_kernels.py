@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--gpu-setup", type=int, default=1, help="SRQCG / aFSAI / Galerkin on the GPU (the identical hierarchy)")
     ap.add_argument("--sets", nargs="*", default=None)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "tune.json"))
+    ap.add_argument("--solves", type=int, default=3, help="timed solves per option set (after one warm-up)")
+    ap.add_argument("--max-it", type=int, default=1000)
     args = ap.parse_args()
     sets = DEFAULT_SETS
     if args.sets:
@@ -51,10 +53,10 @@ def main():
     res = {}
     for name, opts in sets.items():
         g = P.GpuVcycle(h, device=0, options=opts)
-        g.pcg(prob.rhs)  # warm
+        g.pcg(prob.rhs, max_it=args.max_it)  # warm
         t = []
-        for _ in range(3):
-            x, rep = g.pcg(prob.rhs)
+        for _ in range(max(1, args.solves)):
+            x, rep = g.pcg(prob.rhs, max_it=args.max_it)
             t.append(rep.T_s / max(rep.iterations, 1))
         vms = g.time_vcycle(50)
         prof = g.profile_ops(reps=20)
