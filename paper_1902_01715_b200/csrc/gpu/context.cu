@@ -87,12 +87,17 @@ void check_view(const aspamg_csr_view* v, const char* what) {
 // on small operands (< 64k rows, where the longest row's serial chain sets the
 // kernel latency) also <= ~32 sequential entries for the longest row, and
 // widened so the grid still covers the GPU (>= ~150k threads).
-int group_for(double mean, int maxlen, int64_t n_rows, double per_thread = 4.0) {
+// `big_cap`: operands with enough rows to fill the GPU at `big_cap` threads per row
+// (>= ~600k threads) use at most that many: with one warp per row the row sum needs
+// no shared-memory combine and no CTA barrier (ncu, C5 level 1: csr64 at 0.75 of
+// peak with `barrier` the second stall reason).
+int group_for(double mean, int maxlen, int64_t n_rows, double per_thread = 4.0, int big_cap = 256) {
     int g = 1;
     while (g < 256 && per_thread * 2 * g <= mean) g *= 2;
     if (n_rows < 65536)
         while (g < 256 && 32 * g < maxlen) g *= 2;
     while (g < 256 && (double)n_rows * g < 150000.0 && 2.0 * g <= std::max(mean, 1.0)) g *= 2;
+    if (g > big_cap && (double)n_rows * big_cap >= 600000.0) g = big_cap;
     return g;
 }
 
@@ -505,7 +510,8 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr, int
     A.n_rows = (int)v.n_rows;
     A.n_cols = (int)v.n_cols;
     A.nnz = nnz;
-    A.group = group_for(mean, maxlen, v.n_rows, (double)c->opt_csr_per_thread);
+    A.group = group_for(mean, maxlen, v.n_rows, (double)c->opt_csr_per_thread,
+                        (int)std::clamp<long long>(c->opt_csr_max_group, 1, 256));
     A.pf = (int)c->opt_csr_pf;
     if (c->opt_csr_long > 0 && A.group <= 16 && !plain_csr) {
         const int thr = (int)c->opt_csr_long * A.group * 4;
@@ -1138,6 +1144,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "idx16") c->opt_idx16 = value;
         else if (k == "csr_pf") c->opt_csr_pf = value;
         else if (k == "csr_long") c->opt_csr_long = value;
+        else if (k == "csr_max_group") c->opt_csr_max_group = value;
         else if (k == "tail_dense") c->opt_tail_dense = value;
         else if (k == "idx16_max_group") c->opt_idx16_max_group = value;
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;

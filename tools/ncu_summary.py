@@ -27,7 +27,11 @@ def raw_rows(rep):
     else:
         out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
-    return r[0], r[2:]
+    return r[0], r[1], r[2:]
+
+
+UNIT = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6,      # -> MB
+        "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6, "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3, "second": 1e6}   # -> us
 
 
 def ops_from_plain(path):
@@ -75,8 +79,15 @@ def main():
     body = ops[-(len(ops) // 2):] if ops else []  # profile_iter runs the body twice; plain.log prints one
     body = ops
     if args.rep:
-        hdr, rows = raw_rows(args.rep)
+        hdr, units, rows = raw_rows(args.rep)
         g = lambda row, n: row[hdr.index(n)] if n in hdr else ""  # noqa: E731
+
+        def gs(row, n):
+            """Metric scaled by the report's unit for that column (MB for bytes, us for times)."""
+            if n not in hdr:
+                return 0.0
+            i = hdr.index(n)
+            return float(row[i] or 0) * UNIT.get(units[i], 1.0)
         stall_cols = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_")
                       and h.endswith("_per_issue_active.ratio")]
         # align captured kernels with the op sequence (filtered by the capture regex)
@@ -89,9 +100,9 @@ def main():
         traffic = {}
         for k, row in enumerate(rows):
             op = seq[k] if k < len(seq) else ("?", -1, 0, 0)
-            dur = float(g(row, "gpu__time_duration.sum") or 0)  # us
-            rd = float(g(row, "dram__bytes_read.sum") or 0)     # MB
-            wr = float(g(row, "dram__bytes_write.sum") or 0)
+            dur = gs(row, "gpu__time_duration.sum")  # us
+            rd = gs(row, "dram__bytes_read.sum")     # MB
+            wr = gs(row, "dram__bytes_write.sum")
             stalls = sorted(((float(row[i] or 0), hdr[i].replace("smsp__average_warps_issue_stalled_", "")
                               .replace("_per_issue_active.ratio", "")) for i in stall_cols), reverse=True)[:3]
             rec = {"op": op[0], "level": op[1], "kernel": g(row, "Kernel Name").split("(")[0],
