@@ -560,6 +560,8 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr, int
     }
     if (nnz) CK(cudaMemcpy(A.v, v.values, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice));
     A.pol = (long long)(12.0 * nnz) > c->opt_stream_bytes ? 1 : 0;
+    // warp-per-row operands run the column-pipelined kernel (k_csrw)
+    if (c->opt_csrw > 0 && A.group == 32 && !i16 && !A.nlong && !plain_csr) A.wu = c->opt_csrw >= 8 ? 8 : 4;
     return M;
 }
 
@@ -613,7 +615,7 @@ std::string fmt_name(const DMat& M) {
     if (M.fmt == 3) return "xsell" + std::to_string(M.xs.R) + (M.xs.fold == 2 ? "f" : "");
     const std::string base = M.fmt == 1   ? "sbsr3"
                              : M.fmt == 2 ? (M.sell.perm ? "sells" : M.sell.chh == 8 ? "sell8" : "sell")
-                                          : "csr" + std::to_string(M.csr.group);
+                                          : (M.csr.wu ? "csrw" + std::to_string(M.csr.wu) : "csr" + std::to_string(M.csr.group));
     return h ? base + "h" : base;  // h: 16-bit column offsets
 }
 
@@ -1145,6 +1147,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "csr_pf") c->opt_csr_pf = value;
         else if (k == "csr_long") c->opt_csr_long = value;
         else if (k == "csr_max_group") c->opt_csr_max_group = value;
+        else if (k == "csrw") c->opt_csrw = value;
         else if (k == "tail_dense") c->opt_tail_dense = value;
         else if (k == "idx16_max_group") c->opt_idx16_max_group = value;
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;

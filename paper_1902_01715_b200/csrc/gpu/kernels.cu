@@ -339,6 +339,96 @@ __global__ void __launch_bounds__(kBlock) k_csr(DCsr M, int epi, const double* _
     if (red.fin != FIN_NONE) reduce_finish(dacc, red);
 }
 
+// ------------------------------------------------- CSR SpMV, warp per row, pipelined
+// Long-row operands (Galerkin A_l, dense smoother factors: 100..2000 entries per row)
+// with one warp per row. k_csr<32> spends, per row, one memory round trip on the row
+// pointers and TWO per round of 32*U entries (values + columns, then the x gathers that
+// need the columns): at 64 resident warps the dependent chain, not HBM, bounds it (C5
+// level 1: 262 entries per row, 0.75-0.79 of the copy peak). Here the column indices
+// run one round ahead — across row boundaries, the next row's first round is fetched
+// during the current row's last one — and the row pointers two rows ahead, so every
+// round issues its value loads and x gathers together: one round trip per round.
+// Per-lane entry order, fma chain and shuffle tree are those of k_csr<32>: identical bits.
+template <int STREAM, int U>
+__global__ void __launch_bounds__(kBlock) k_csrw(DCsr M, int epi, const double* __restrict__ x, double* y,
+                                                  const double* aux, double omega, const double* dotw, Red red,
+                                                  const int* done) {
+    pdl_enter();
+    if (is_done(done)) return;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * kBlock) >> 5;
+    double dacc = 0.0;
+    int row = warp;
+    int b = 0, e = 0, nb = 0, ne = 0;
+    int cn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cn[u] = 0;
+    if (row < M.n_rows) {
+        b = __ldg(M.rp + row);
+        e = __ldg(M.rp + row + 1);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int k = b + lane + 32 * u;
+            cn[u] = k < e ? ld_mat<STREAM>(M.ci + k) : 0;
+        }
+        if (row + nwarps < M.n_rows) {
+            nb = __ldg(M.rp + row + nwarps);
+            ne = __ldg(M.rp + row + nwarps + 1);
+        }
+    }
+    while (row < M.n_rows) {
+        const int nrow = row + nwarps;
+        int fb = 0, fe = 0;  // pointers of the row after next
+        if (nrow + nwarps < M.n_rows) {
+            fb = __ldg(M.rp + nrow + nwarps);
+            fe = __ldg(M.rp + nrow + nwarps + 1);
+        }
+        double s = 0.0;
+        int k0 = b + lane;
+        do {  // at least one pass: an empty row still fetches the next row's first columns
+            double v[U], xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = k0 + 32 * u;
+                const bool p = k < e;
+                v[u] = p ? ld_mat<STREAM>(M.v + k) : 0.0;
+                xv[u] = p ? __ldg(x + cn[u]) : 0.0;
+            }
+            const int kn = k0 + 32 * U;
+            if (kn - lane < e) {  // warp-uniform: another round of this row
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = kn + 32 * u;
+                    cn[u] = k < e ? ld_mat<STREAM>(M.ci + k) : 0;
+                }
+            } else if (nrow < M.n_rows) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = nb + lane + 32 * u;
+                    cn[u] = k < ne ? ld_mat<STREAM>(M.ci + k) : 0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) s = fma(v[u], xv[u], s);
+            k0 = kn;
+        } while (k0 - lane < e);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            const double out = epilogue(epi, s, aux, row, omega);
+            y[row] = out;
+            if (dotw) dacc = fma(out, dotw[row], dacc);
+        }
+        row = nrow;
+        b = nb;
+        e = ne;
+        nb = fb;
+        ne = fe;
+    }
+    if (red.fin != FIN_NONE) reduce_finish(dacc, red);
+}
+
 constexpr int SB_U = 3;    // block slots per load group (sliced BSR3)
 
 // ------------------------------------------------------- sliced BSR3 SpMV
@@ -1014,6 +1104,11 @@ SpmvKern csr_kernel(const DCsr& A) {
     return A.ci16 ? csr_kernel_i<GG, P, true>(A) : csr_kernel_i<GG, P, false>(A);
 }
 #define CSRK(GG, P) csr_kernel<GG, P>(M.csr)
+// Warp-per-row pipelined variant (DCsr::wu = columns fetched per lane per round, 4 or 8).
+SpmvKern csrw_kernel(const DCsr& A) {
+    if (A.wu >= 8) return A.pol == 1 ? k_csrw<1, 8> : A.pol == 2 ? k_csrw<2, 8> : k_csrw<0, 8>;
+    return A.pol == 1 ? k_csrw<1, 4> : A.pol == 2 ? k_csrw<2, 4> : k_csrw<0, 4>;
+}
 using XsellKern = void (*)(DXsell, int, const double*, double*, const double*, double, const double*, Red, const int*);
 XsellKern xsell_kernel(const DXsell& X) {
 #define ASPAMG_XS(QQ, MB)                                                                              \
@@ -1055,6 +1150,7 @@ int spmv_grid(const DMat& M) {
     const int T = M.csr.group;
     const long long ctas = ((long long)M.csr.n_rows * T + kBlock - 1) / kBlock;
     const int st = M.csr.pol;
+    if (M.csr.wu) return occ_grid(csrw_kernel(M.csr), ctas);
     // + the long-row CTAs (M.csr.nlctas, fixed at upload) ahead of the regular grid
 #define ASPAMG_CSR_OCC(TT)                                                                                   \
     case TT: return M.csr.nlctas + (st == 1 ? occ_grid(CSRK(TT, 1), ctas)                                    \
@@ -1107,6 +1203,10 @@ void spmv(const DMat& M, Epi epi, const double* x, double* y, const double* aux,
         ASPAMG_SELL(4, 4)
         ASPAMG_SELL(2, 1)
 #undef ASPAMG_SELL
+        return;
+    }
+    if (M.csr.wu) {
+        launch(csrw_kernel(M.csr), grid, kBlock, 0, L.stream, M.csr, epi, x, y, aux, omega, dotw, red, done);
         return;
     }
 #define ASPAMG_CSR_CASE(GG)                                                                                   \

@@ -28,6 +28,7 @@ struct DCsr {
     unsigned short* ci16 = nullptr;
     int* cb = nullptr;
     int pf = 0;  // k_csr row-pointer prefetch (T <= 16)
+    int wu = 0;  // > 0: warp-per-row pipelined kernel k_csrw (group == 32, 32-bit columns), wu columns per lane per round
     // Long-row split: rows longer than lthr (listed in lrows) are computed by the
     // first nlctas CTAs of the launch, one warp per row; the regular T-thread
     // groups skip them, so a long-tailed operand (G' rows up to ~7x the mean) no

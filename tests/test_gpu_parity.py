@@ -458,6 +458,85 @@ def test_sell_all_empty_row_groups(pkg):
         lib.aspamg_gpu_ctx_destroy(ctx)
 
 
+@pytest.mark.parametrize("u", [4, 8])
+def test_csrw_pipelined_kernel_bit_identical(pkg, oracle, u):
+    """Warp-per-row pipelined CSR kernel (k_csrw: columns one round ahead across row
+    boundaries, row pointers two rows ahead): same per-lane order, fma chain and shuffle
+    tree as k_csr<32>, so every product and the whole V-cycle are bit-identical to the
+    unpipelined kernel with the same thread groups; PCG inside the north_star gates."""
+    p, h = problem_and_hierarchy(2, 2)
+    base = dict(csr_max_group=32, csr_per_thread=1, sell_min_rows=1 << 40, csr_long=0, idx16=0)
+    g0 = _gpu(pkg, h, csrw=0, **base)
+    g1 = _gpu(pkg, h, csrw=u, **base)
+    o = _oracle(oracle, h)
+    names = [n for n, l, _, _ in g1.profile_iteration()]
+    assert sum(".csrw" in n for n in names) >= 2, names
+    rng = np.random.default_rng(31)
+    for l in range(h.n_levels - 1):
+        for wi, which in enumerate(["A", "G", "Gt", "P", "Pt"]):
+            m = getattr(h.level(l, copy=False), which)
+            x = rng.standard_normal(m.n_cols)
+            assert np.array_equal(g1.spmv(l, wi, x), g0.spmv(l, wi, x)), (which, l)
+    y = rng.standard_normal(p.K.n_rows)
+    assert np.array_equal(g1.apply(y), g0.apply(y))
+    assert rel_err(g1.apply(y), o.vcycle(y)) < RTOL_VCYCLE
+    _pcg_parity(p, h, g1, o)
+    g0.close()
+    g1.close()
+
+
+@pytest.mark.parametrize("u", [4, 8])
+def test_csrw_ragged_and_empty_rows(pkg, u):
+    """k_csrw on an operand with empty rows (single and in long runs, first and last
+    row), rows of exactly one round, one entry more, and many rounds, with more rows
+    than resident warps: exact products (small integers) against scipy."""
+    import ctypes as C
+    import scipy.sparse as sp
+    from paper_1902_01715_b200 import _native as N
+    lib = N.gpu()
+    rng = np.random.default_rng(37)
+    n, nc = 70000, 3000
+    lens = rng.choice([0, 0, 1, 31, 32, 33, 32 * u, 32 * u + 1, 200, 700], size=n)
+    lens[0] = 0
+    lens[-1] = 0
+    lens[1000:1400] = 0  # a run of empty rows longer than one warp stride window
+    lens[5] = 2500
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    ci = np.concatenate([np.sort(rng.choice(nc, size=k, replace=False)) for k in lens if k] or [np.zeros(0, np.int64)])
+    va = rng.integers(-3, 4, size=rp[-1]).astype(float)
+    Pm = sp.csr_matrix((va, ci.astype(np.int64), rp), shape=(n, nc))
+    I = sp.identity(n, format="csr")
+    Ic = sp.identity(nc, format="csr")
+    mats0 = [pkg.SparseMatrix.from_scipy(m) for m in (I, I, I, Pm, Pm.T.tocsr())]
+    empty = pkg.SparseMatrix(0, 0, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    mats1 = [pkg.SparseMatrix.from_scipy(Ic)] + [empty] * 4
+    ctx = C.c_void_p()
+    assert lib.aspamg_gpu_ctx_create(0, C.byref(ctx)) == 0
+    try:
+        for k, v in {"sell_min_rows": 1 << 40, "bsr": 0, "tail_dense": 0, "csr_long": 0, "idx16": 0, "csrw": u,
+                     "csr_per_thread": 1, "csr_max_group": 32}.items():
+            assert lib.aspamg_gpu_set_option(ctx, k.encode(), v) == 0
+        for l, ms in enumerate((mats0, mats1)):
+            views = [m.view() for m in ms]
+            assert lib.aspamg_gpu_upload_level(ctx, l, *[C.byref(v) for v in views], 1.0) == 0
+        L = np.ascontiguousarray(np.eye(nc).ravel(order="F"))
+        assert lib.aspamg_gpu_upload_coarse(ctx, nc, L.ctypes.data_as(C.POINTER(C.c_double))) == 0
+        assert lib.aspamg_gpu_finalize(ctx) == 0
+        cap, cnt = 64, C.c_int()
+        buf = (N.GpuKernelTime * cap)()
+        assert lib.aspamg_gpu_profile_iteration(ctx, buf, cap, C.byref(cnt)) == 0
+        names = [buf[i].name.decode() for i in range(cnt.value)]
+        assert any(nm.startswith("prolong_P.csrw") for nm in names), names
+        x = rng.integers(-4, 5, size=nc).astype(float)
+        y = np.empty(n)
+        P_d = C.POINTER(C.c_double)
+        assert lib.aspamg_gpu_spmv(ctx, 0, 3, x.ctypes.data_as(P_d), y.ctypes.data_as(P_d)) == 0
+        assert np.array_equal(y, Pm @ x)
+    finally:
+        lib.aspamg_gpu_ctx_destroy(ctx)
+
+
 def test_upload_rejects_unsorted_row(pkg):
     """check_view: columns must ascend within a row (sparse_matrix.hpp:27-33) —
     the 16-bit column mode would otherwise wrap silently. Status 1 (DimensionError)."""
