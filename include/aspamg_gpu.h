@@ -43,7 +43,7 @@ typedef struct aspamg_gpu_ctx aspamg_gpu_ctx;
 
 typedef struct aspamg_gpu_level_stats {
     int64_t n;
-    int32_t a_format;     /* 0 CSR warp-per-row, 1 sliced 3x3 BSR, 2 SELL-32 */
+    int32_t a_format;     /* 0 CSR (thread group per row), 1 sliced 3x3 BSR, 2 SELL-32, 3 tile-local SELL */
     int64_t a_nnz, a_nnzb;
     double a_fill;        /* stored values / true nnz (1.0 = exact) */
     int64_t g_nnz, p_nnz;
@@ -72,14 +72,23 @@ int aspamg_gpu_ctx_destroy(aspamg_gpu_ctx* ctx);
  *   "keep_bytes"   coarsest levels up to this many bytes load with evict-last
  *   "coarse_mode"  1 explicit inverse-factor triangles (default), 0 one-CTA substitution
  *   "idx16"        16-bit column offsets where rows span < 2^16 columns (default 1)
- *   "sell_*"       SELL layout / kernel choices (chunk height, sorting window, unroll, TMA ring)
- *   "csr_per_thread", "csr_u8", "csr_pf", "csr_long"  CSR kernel group size, loads per round,
- *                  row-pointer prefetch (default on), long-row split threshold (0 = off)
- *   "rseg", "rseg_u", "rseg_max_mean", "rseg_min_rows"  row-segment kernel (off by default)
+ *   "sell_*"       SELL layout / kernel choices (chunk height, sorting window, unroll)
+ *   "csr_per_thread", "csr_pf", "csr_long"  CSR kernel group size (entries per thread of the
+ *                  mean row), row-pointer prefetch (1 = groups <= 16, default; 2 = also warp-per-row),
+ *                  long-row split threshold (0 = off)
+ *   "csr_max_group" (32) threads per row cap for operands with >= 600k / cap rows: one warp per
+ *                  row, no shared-memory combine
+ *   "csrw"         (4) pipelined warp-per-row CSR kernel for group-32 operands: column indices one
+ *                  round ahead across row boundaries; value = columns per lane per round (4 / 8), 0 off
+ *   "xsell", "xsell_*"  tile-local SELL (x footprint staged in shared memory, 16-bit local columns):
+ *                  role mask (1 A, 2 G, 4 G', 8 P, 16 P'; default 0 = off) and its layout choices
+ *   "fuse_rr"      (0) restriction fused with the residual: one cooperative launch per level computes
+ *                  r = y - A s, crosses a grid barrier, gathers r_c = P' r (measured slower)
+ *   "tail_dense"   (1500) levels below the first one with <= this many rows collapse into one dense operator
  *   "tail_rows"    levels below this many rows run as one persistent cooperative kernel (0 = off)
  *   "pdl"          programmatic dependent launch (default 1)
- * Every variant sums in a fixed order (deterministic); sliced / row-segment
- * formats are bit-identical to the reference spmv (tests/test_gpu_parity.py). */
+ * Every variant sums in a fixed order (deterministic); the sliced formats (BSR3, SELL, tile-local
+ * SELL) are bit-identical to the reference spmv (tests/test_gpu_parity.py). */
 int aspamg_gpu_set_option(aspamg_gpu_ctx* ctx, const char* key, int64_t value);
 int aspamg_gpu_set_cycle(aspamg_gpu_ctx* ctx, int64_t nu1, int64_t nu2);
 /* Levels 0..L-2 carry A, G, G', P, P' and omega; the coarsest level L-1 carries

@@ -402,7 +402,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr, int
     // which walks plain CSR rows — P' then skips the sliced formats and the long-row split
     const bool plain_csr = role == 4 && c->opt_fuse_rr;
     if (!plain_csr && role >= 0 && ((c->opt_xsell >> role) & 1) && v.n_rows >= c->opt_xsell_min_rows &&
-        mean <= (double)c->opt_xsell_max_mean && build_xsell(c, v, M.xs)) {
+        mean <= (double)c->opt_xsell_max_mean && mean >= (double)c->opt_xsell_min_mean && build_xsell(c, v, M.xs)) {
         M.fmt = 3;
         return M;
     }
@@ -1162,6 +1162,7 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "xsell") c->opt_xsell = value;
         else if (k == "xsell_min_rows") c->opt_xsell_min_rows = value;
         else if (k == "xsell_max_mean") c->opt_xsell_max_mean = value;
+        else if (k == "xsell_min_mean") c->opt_xsell_min_mean = value;
         else if (k == "xsell_rows") c->opt_xsell_rows = value;
         else if (k == "xsell_fold") c->opt_xsell_fold = value;
         else if (k == "xsell_rows256") c->opt_xsell_rows256 = value;

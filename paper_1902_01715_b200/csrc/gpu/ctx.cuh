@@ -76,14 +76,14 @@ struct aspamg_gpu_ctx {
     // lane (fold: 1, or 2 = long rows paired with short ones; a tile has threads x fold rows),
     // footprint granule (log2 doubles), kernel variant (quads per group x 10 + min CTAs/SM),
     // shared-memory budget per CTA.
-    long long opt_xsell = 0, opt_xsell_min_rows = 32768, opt_xsell_max_mean = 256, opt_xsell_rows = 0,
+    long long opt_xsell = 0, opt_xsell_min_rows = 32768, opt_xsell_max_mean = 256, opt_xsell_min_mean = 0, opt_xsell_rows = 0,
               opt_xsell_rows256 = 400000, opt_xsell_rows128 = 100000, opt_xsell_gran = 3, opt_xsell_q = 0,
               opt_xsell_smem_kb = 100, opt_xsell_fold = 2;
     // collapse the V-cycle below the first level with <= this many rows (0 = off);
     // C2 0.995 -> 0.966 ms/it, C1 0.120 -> 0.107 ms/it (profiles/tune_r01_tail_long.log)
     long long opt_tail_dense = 1500;
-    long long opt_csrw = 0;  // warp-per-row pipelined CSR kernel for group == 32 operands: columns per lane per round (4 / 8), 0 = off
-    long long opt_csr_max_group = 256;  // threads per row cap for operands with >= 600k / cap rows
+    long long opt_csrw = 4;  // warp-per-row pipelined CSR kernel for group == 32 operands: columns per lane per round (4 / 8), 0 = off
+    long long opt_csr_max_group = 32;  // threads per row cap for operands with >= 600k / cap rows
     long long opt_fuse_rr = 0;  // restriction fused with the residual (one cooperative launch per level)
     long long opt_csr_long = 4;  // long-row split threshold in rounds (rows > long*T*4 entries; 0 = off)
     long long opt_csr_pf = 1;  // CSR (T <= 16): prefetch the next row's pointers (measured 1.4% faster per PCG iteration on C2)

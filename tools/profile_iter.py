@@ -34,6 +34,9 @@ def main():
     g = P.GpuVcycle(h, device=0, options=opts)
     # ncu runs this with --profile-from-start off: only the two body runs below are
     # captured (not the upload / finalize kernels, e.g. the dense-tail probe).
+    # a short real solve first: the profiled iteration then runs on live vectors (on a fresh
+    # context r = p = 0, p'Kp = 0 raises the not-SPD flag and the last op, pcg_xr, returns early)
+    g.pcg(prob.rhs, max_it=3)
     import ctypes
     cu = ctypes.CDLL("libcuda.so.1")
     cu.cuProfilerStart()
