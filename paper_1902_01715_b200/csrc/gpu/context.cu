@@ -561,7 +561,11 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr, int
     if (nnz) CK(cudaMemcpy(A.v, v.values, (size_t)nnz * sizeof(double), cudaMemcpyHostToDevice));
     A.pol = (long long)(12.0 * nnz) > c->opt_stream_bytes ? 1 : 0;
     // warp-per-row operands run the column-pipelined kernel (k_csrw)
-    if (c->opt_csrw > 0 && A.group == 32 && !i16 && !A.nlong && !plain_csr) A.wu = c->opt_csrw >= 8 ? 8 : 4;
+    if (c->opt_csrw > 0 && A.group == 32 && !i16 && !A.nlong && !plain_csr) {
+        A.wu = c->opt_csrw >= 8 ? 8 : 4;
+        if (A.pol == 1 && c->opt_csr_noalloc) A.pol = 3;  // streamed operand: matrix loads bypass L1
+        A.blk = c->opt_csr_blocked ? 1 : 0;
+    }
     return M;
 }
 
@@ -1148,6 +1152,8 @@ int aspamg_gpu_set_option(aspamg_gpu_ctx* c, const char* key, int64_t value) {
         else if (k == "csr_long") c->opt_csr_long = value;
         else if (k == "csr_max_group") c->opt_csr_max_group = value;
         else if (k == "csrw") c->opt_csrw = value;
+        else if (k == "csr_noalloc") c->opt_csr_noalloc = value;
+        else if (k == "csr_blocked") c->opt_csr_blocked = value;
         else if (k == "tail_dense") c->opt_tail_dense = value;
         else if (k == "idx16_max_group") c->opt_idx16_max_group = value;
         else if (k == "sell_max_mean") c->opt_sell_max_mean = value;

@@ -82,6 +82,8 @@ struct aspamg_gpu_ctx {
     // collapse the V-cycle below the first level with <= this many rows (0 = off);
     // C2 0.995 -> 0.966 ms/it, C1 0.120 -> 0.107 ms/it (profiles/tune_r01_tail_long.log)
     long long opt_tail_dense = 1500;
+    long long opt_csr_blocked = 0;  // k_csrw: contiguous row block per CTA
+    long long opt_csr_noalloc = 0;  // k_csrw on streamed operands: matrix loads with L1::no_allocate
     long long opt_csrw = 4;  // warp-per-row pipelined CSR kernel for group == 32 operands: columns per lane per round (4 / 8), 0 = off
     long long opt_csr_max_group = 32;  // threads per row cap for operands with >= 600k / cap rows
     long long opt_fuse_rr = 0;  // restriction fused with the residual (one cooperative launch per level)

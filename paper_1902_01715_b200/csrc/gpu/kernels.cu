@@ -180,9 +180,47 @@ __device__ __forceinline__ uint2 ld_keep(const uint2* p) {
     asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(l2_keep_policy()));
     return r;
 }
+// POL 3: stream past L1 (no_allocate) with an L2 evict-first hint — the matrix stream of the
+// warp-per-row kernels then leaves L1 to the x gathers.
+__device__ __forceinline__ unsigned long long l2_first_policy() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double ld_na(const double* p) {
+    double r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(l2_first_policy()));
+    return r;
+}
+__device__ __forceinline__ int ld_na(const int* p) {
+    int r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(l2_first_policy()));
+    return r;
+}
+__device__ __forceinline__ double ld_na(const double* p, unsigned long long pol) {
+    double r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int ld_na(const int* p, unsigned long long pol) {
+    int r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_hint(const double* p, unsigned long long pol) {
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int ld_hint(const int* p, unsigned long long pol) {
+    int r;
+    asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
 template <int POL, class T>
 __device__ __forceinline__ T ld_mat(const T* p) {
-    if constexpr (POL == 1) return __ldcs(p);
+    if constexpr (POL == 3) return ld_na(p);
+    else if constexpr (POL == 1) return __ldcs(p);
     else if constexpr (POL == 2) return ld_keep(p);
     else return __ldg(p);
 }
@@ -355,32 +393,52 @@ __global__ void __launch_bounds__(kBlock) k_csrw(DCsr M, int epi, const double* 
                                                   const int* done) {
     pdl_enter();
     if (is_done(done)) return;
+    // one L2 policy per thread, not per load
+    const unsigned long long hint = STREAM == 3 ? l2_first_policy() : STREAM == 2 ? l2_keep_policy() : 0ull;
+    auto ldm = [&](auto* p) {
+        if constexpr (STREAM == 3) return ld_na(p, hint);
+        else if constexpr (STREAM == 2) return ld_hint(p, hint);
+        else return ld_mat<STREAM>(p);
+    };
     const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * kBlock) >> 5;
+    // Row assignment. Interleaved (blk = 0): warp w takes rows w, w + nwarps, ... Blocked (blk = 1):
+    // CTA b owns the contiguous rows [b * rpc, (b + 1) * rpc) and its 8 warps walk them together,
+    // 8 adjacent rows per step — the x lines one step gathers are reused by the next steps of the
+    // same CTA out of L1 (neighbouring rows share most of their columns).
+    int row, n_end, nwarps;
+    if (M.blk) {
+        constexpr int wpc = kBlock / 32;
+        const int rpc = (((M.n_rows + (int)gridDim.x - 1) / (int)gridDim.x + wpc - 1) / wpc) * wpc;
+        row = min((long long)blockIdx.x * rpc, (long long)M.n_rows) + (threadIdx.x >> 5);
+        n_end = (int)min((long long)(blockIdx.x + 1) * rpc, (long long)M.n_rows);
+        nwarps = wpc;
+    } else {
+        row = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+        n_end = M.n_rows;
+        nwarps = (gridDim.x * kBlock) >> 5;
+    }
     double dacc = 0.0;
-    int row = warp;
     int b = 0, e = 0, nb = 0, ne = 0;
     int cn[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) cn[u] = 0;
-    if (row < M.n_rows) {
+    if (row < n_end) {
         b = __ldg(M.rp + row);
         e = __ldg(M.rp + row + 1);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int k = b + lane + 32 * u;
-            cn[u] = k < e ? ld_mat<STREAM>(M.ci + k) : 0;
+            cn[u] = k < e ? ldm(M.ci + k) : 0;
         }
-        if (row + nwarps < M.n_rows) {
+        if (row + nwarps < n_end) {
             nb = __ldg(M.rp + row + nwarps);
             ne = __ldg(M.rp + row + nwarps + 1);
         }
     }
-    while (row < M.n_rows) {
+    while (row < n_end) {
         const int nrow = row + nwarps;
         int fb = 0, fe = 0;  // pointers of the row after next
-        if (nrow + nwarps < M.n_rows) {
+        if (nrow + nwarps < n_end) {
             fb = __ldg(M.rp + nrow + nwarps);
             fe = __ldg(M.rp + nrow + nwarps + 1);
         }
@@ -392,7 +450,7 @@ __global__ void __launch_bounds__(kBlock) k_csrw(DCsr M, int epi, const double* 
             for (int u = 0; u < U; ++u) {
                 const int k = k0 + 32 * u;
                 const bool p = k < e;
-                v[u] = p ? ld_mat<STREAM>(M.v + k) : 0.0;
+                v[u] = p ? ldm(M.v + k) : 0.0;
                 xv[u] = p ? __ldg(x + cn[u]) : 0.0;
             }
             const int kn = k0 + 32 * U;
@@ -400,13 +458,13 @@ __global__ void __launch_bounds__(kBlock) k_csrw(DCsr M, int epi, const double* 
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int k = kn + 32 * u;
-                    cn[u] = k < e ? ld_mat<STREAM>(M.ci + k) : 0;
+                    cn[u] = k < e ? ldm(M.ci + k) : 0;
                 }
-            } else if (nrow < M.n_rows) {
+            } else if (nrow < n_end) {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int k = nb + lane + 32 * u;
-                    cn[u] = k < ne ? ld_mat<STREAM>(M.ci + k) : 0;
+                    cn[u] = k < ne ? ldm(M.ci + k) : 0;
                 }
             }
 #pragma unroll
@@ -1106,6 +1164,7 @@ SpmvKern csr_kernel(const DCsr& A) {
 #define CSRK(GG, P) csr_kernel<GG, P>(M.csr)
 // Warp-per-row pipelined variant (DCsr::wu = columns fetched per lane per round, 4 or 8).
 SpmvKern csrw_kernel(const DCsr& A) {
+    if (A.pol == 3) return A.wu >= 8 ? k_csrw<3, 8> : k_csrw<3, 4>;
     if (A.wu >= 8) return A.pol == 1 ? k_csrw<1, 8> : A.pol == 2 ? k_csrw<2, 8> : k_csrw<0, 8>;
     return A.pol == 1 ? k_csrw<1, 4> : A.pol == 2 ? k_csrw<2, 4> : k_csrw<0, 4>;
 }
@@ -1150,7 +1209,11 @@ int spmv_grid(const DMat& M) {
     const int T = M.csr.group;
     const long long ctas = ((long long)M.csr.n_rows * T + kBlock - 1) / kBlock;
     const int st = M.csr.pol;
-    if (M.csr.wu) return occ_grid(csrw_kernel(M.csr), ctas);
+    if (M.csr.wu) {
+        const int g = occ_grid(csrw_kernel(M.csr), ctas);
+        // blocked rows: 4 waves of CTAs, so uneven row blocks still balance over the SMs
+        return M.csr.blk ? (int)(4ll * g < ctas ? 4ll * g : ctas) : g;
+    }
     // + the long-row CTAs (M.csr.nlctas, fixed at upload) ahead of the regular grid
 #define ASPAMG_CSR_OCC(TT)                                                                                   \
     case TT: return M.csr.nlctas + (st == 1 ? occ_grid(CSRK(TT, 1), ctas)                                    \

@@ -28,6 +28,7 @@ struct DCsr {
     unsigned short* ci16 = nullptr;
     int* cb = nullptr;
     int pf = 0;  // k_csr row-pointer prefetch (T <= 16)
+    int blk = 0; // k_csrw: 1 = contiguous row block per CTA (L1 reuse of x across steps), 0 = rows interleaved over the grid
     int wu = 0;  // > 0: warp-per-row pipelined kernel k_csrw (group == 32, 32-bit columns), wu columns per lane per round
     // Long-row split: rows longer than lthr (listed in lrows) are computed by the
     // first nlctas CTAs of the launch, one warp per row; the regular T-thread

@@ -458,8 +458,9 @@ def test_sell_all_empty_row_groups(pkg):
         lib.aspamg_gpu_ctx_destroy(ctx)
 
 
-@pytest.mark.parametrize("u", [4, 8])
-def test_csrw_pipelined_kernel_bit_identical(pkg, oracle, u):
+@pytest.mark.parametrize("u,extra", [(4, {}), (8, {}), (4, {"csr_blocked": 1}), (8, {"csr_blocked": 1, "csr_noalloc": 1,
+                                                                                  "stream_bytes": 1})])
+def test_csrw_pipelined_kernel_bit_identical(pkg, oracle, u, extra):
     """Warp-per-row pipelined CSR kernel (k_csrw: columns one round ahead across row
     boundaries, row pointers two rows ahead): same per-lane order, fma chain and shuffle
     tree as k_csr<32>, so every product and the whole V-cycle are bit-identical to the
@@ -467,7 +468,7 @@ def test_csrw_pipelined_kernel_bit_identical(pkg, oracle, u):
     p, h = problem_and_hierarchy(2, 2)
     base = dict(csr_max_group=32, csr_per_thread=1, sell_min_rows=1 << 40, csr_long=0, idx16=0)
     g0 = _gpu(pkg, h, csrw=0, **base)
-    g1 = _gpu(pkg, h, csrw=u, **base)
+    g1 = _gpu(pkg, h, csrw=u, **base, **extra)  # blocked rows / L1-bypassing matrix loads change no bits
     o = _oracle(oracle, h)
     names = [n for n, l, _, _ in g1.profile_iteration()]
     assert sum(".csrw" in n for n in names) >= 2, names
@@ -485,8 +486,8 @@ def test_csrw_pipelined_kernel_bit_identical(pkg, oracle, u):
     g1.close()
 
 
-@pytest.mark.parametrize("u", [4, 8])
-def test_csrw_ragged_and_empty_rows(pkg, u):
+@pytest.mark.parametrize("u,blocked", [(4, 0), (8, 0), (4, 1), (8, 1)])
+def test_csrw_ragged_and_empty_rows(pkg, u, blocked):
     """k_csrw on an operand with empty rows (single and in long runs, first and last
     row), rows of exactly one round, one entry more, and many rounds, with more rows
     than resident warps: exact products (small integers) against scipy."""
@@ -515,7 +516,8 @@ def test_csrw_ragged_and_empty_rows(pkg, u):
     assert lib.aspamg_gpu_ctx_create(0, C.byref(ctx)) == 0
     try:
         for k, v in {"sell_min_rows": 1 << 40, "bsr": 0, "tail_dense": 0, "csr_long": 0, "idx16": 0, "csrw": u,
-                     "csr_per_thread": 1, "csr_max_group": 32}.items():
+                     "csr_per_thread": 1, "csr_max_group": 32, "csr_blocked": blocked, "csr_noalloc": blocked,
+                     "stream_bytes": 1 if blocked else 48 << 20}.items():
             assert lib.aspamg_gpu_set_option(ctx, k.encode(), v) == 0
         for l, ms in enumerate((mats0, mats1)):
             views = [m.view() for m in ms]
