@@ -442,8 +442,10 @@ def run_b200(args, ws, rank, local):
                    "rel_tol": args.tol, "K_format": "bsr3" if lv0.a_format == 1 else "csr",
                    "setup_s": t_setup, "setup_on": origin,
                    "upload_s": t_upload, "parallelism": f"replicas x{ws}",
-                   "vcycle": "V(1,1), levels below the first with <= 1500 rows collapsed into one dense operator "
-                             "formed on the device at upload (tail_dense); CSR long rows split to warp-per-row CTAs",
+                   "vcycle": "V(1,1); K sliced BSR3, short-row operands SELL / CSR, long-row operands one warp per row "
+                             "(column-pipelined k_csrw, contiguous row blocks per CTA on >= 250k-row operands); levels "
+                             "below the first with <= 1500 rows collapsed into one dense operator formed on the device "
+                             "at upload (tail_dense)",
                    "l2": "inputs larger than L2 (K alone > 126 MB), no flush" if args.config != 1 else "K fits in L2"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_note, "kernel": top[0], "level": top[1],

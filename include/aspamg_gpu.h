@@ -80,6 +80,9 @@ int aspamg_gpu_ctx_destroy(aspamg_gpu_ctx* ctx);
  *                  row, no shared-memory combine
  *   "csrw"         (4) pipelined warp-per-row CSR kernel for group-32 operands: column indices one
  *                  round ahead across row boundaries; value = columns per lane per round (4 / 8), 0 off
+ *   "csr_blocked"  (250000) k_csrw operands with at least this many rows: a contiguous row block per
+ *                  CTA instead of rows interleaved over the grid (L1 reuse of the x gathers); 0 = off
+ *   "csr_noalloc"  (0) k_csrw matrix loads bypass L1 (measured slower)
  *   "xsell", "xsell_*"  tile-local SELL (x footprint staged in shared memory, 16-bit local columns):
  *                  role mask (1 A, 2 G, 4 G', 8 P, 16 P'; default 0 = off) and its layout choices
  *   "fuse_rr"      (0) restriction fused with the residual: one cooperative launch per level computes

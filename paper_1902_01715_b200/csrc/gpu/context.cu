@@ -564,7 +564,7 @@ DMat upload_mat(aspamg_gpu_ctx* c, const aspamg_csr_view& v, bool allow_bsr, int
     if (c->opt_csrw > 0 && A.group == 32 && !i16 && !A.nlong && !plain_csr) {
         A.wu = c->opt_csrw >= 8 ? 8 : 4;
         if (A.pol == 1 && c->opt_csr_noalloc) A.pol = 3;  // streamed operand: matrix loads bypass L1
-        A.blk = c->opt_csr_blocked ? 1 : 0;
+        A.blk = (c->opt_csr_blocked > 0 && v.n_rows >= c->opt_csr_blocked) ? 1 : 0;
     }
     return M;
 }

@@ -82,7 +82,10 @@ struct aspamg_gpu_ctx {
     // collapse the V-cycle below the first level with <= this many rows (0 = off);
     // C2 0.995 -> 0.966 ms/it, C1 0.120 -> 0.107 ms/it (profiles/tune_r01_tail_long.log)
     long long opt_tail_dense = 1500;
-    long long opt_csr_blocked = 0;  // k_csrw: contiguous row block per CTA
+    // k_csrw: operands with at least this many rows give every CTA a contiguous row block (x lines
+    // gathered for rows r..r+7 are reused from L1 by the CTA's next steps); 0 = off. C5: 10.35 -> 10.01
+    // ms/it (level-1/2 operands -3..-8 %); C2's 168k-row A_1 is 3 % slower with it, hence the threshold.
+    long long opt_csr_blocked = 250000;
     long long opt_csr_noalloc = 0;  // k_csrw on streamed operands: matrix loads with L1::no_allocate
     long long opt_csrw = 4;  // warp-per-row pipelined CSR kernel for group == 32 operands: columns per lane per round (4 / 8), 0 = off
     long long opt_csr_max_group = 32;  // threads per row cap for operands with >= 600k / cap rows
