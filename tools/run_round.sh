@@ -1,17 +1,24 @@
-# One GPU session: tests, smoke, bench (both arms), then ncu captures.
-cd $GRAFT_REPO_ROOT
+#!/bin/bash
+# One GPU session in the driver's order (tests, smoke, reference arm, GPU arm) on a
+# cold box, then the ncu evidence for every launch of one iteration on C5 and C2.
+cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
-nvidia-smi > gpurun_out/nvsmi.txt 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 1500 python -m pytest tests/ -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?" >> gpurun_out/bench_ref.err
-python tools/profile_iter.py > gpurun_out/plain.log 2>&1 && \
-ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/profile_iter.py > gpurun_out/ncu_list.log 2>&1
-echo "list rc=$?" >> gpurun_out/ncu_list.log
-python tools/profile_iter.py > gpurun_out/plain2.log 2>&1
-# skip the warm-up iteration's SpMV-family launches (one per SpMV op line of the op table)
-SKIP=$(grep -cE "^(smooth|resid|restrict|prolong|pcg_Kp|coarse_|tail_dense)" gpurun_out/plain2.log)
-echo "skip=$SKIP" > gpurun_out/ncu_skip.txt
-ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"k_sbsr3|k_csr|k_sell" -s $SKIP -c 8 -o gpurun_out/prof_full python tools/profile_iter.py > gpurun_out/ncu_full.log 2>&1
-echo "full rc=$?" >> gpurun_out/ncu_full.log
+O=gpurun_out
+TAG=${TAG:-r02}
+STEPS="${1:-tests smoke c5ref c5 prof5 prof2 c2 asm}"
+{ nvidia-smi; free -g; nproc; lscpu | grep "Model name"; } > $O/box_d.txt 2>&1
+for s in $STEPS; do
+  t0=$(date +%s)
+  case $s in
+    tests) timeout 2400 python -m pytest tests/ -q -m gpu --durations=8 > $O/pytest_gpu_d.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu_d.log ;;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke_d.log 2>&1; echo "smoke rc=$?" >> $O/smoke_d.log ;;
+    c5ref) timeout 2400 python bench.py --impl reference > $O/bench_${TAG}_c5_reference.json 2> $O/bench_c5_ref_d.err; echo "rc=$?" >> $O/bench_c5_ref_d.err ;;
+    c5) timeout 2400 python bench.py > $O/bench_${TAG}_c5.json 2> $O/bench_c5_d.err; echo "rc=$?" >> $O/bench_c5_d.err ;;
+    c2) timeout 900 python bench.py --config 2 > $O/bench_${TAG}_c2.json 2> $O/bench_c2_d.err; echo "rc=$?" >> $O/bench_c2_d.err
+        timeout 900 python bench.py --config 2 --impl reference > $O/bench_${TAG}_c2_reference.json 2>> $O/bench_c2_d.err ;;
+    prof5) timeout 2400 bash tools/run_profile.sh 5 ${TAG}_c5 > $O/prof5_d.log 2>&1 ;;
+    prof2) timeout 1500 bash tools/run_profile.sh 2 ${TAG}_c2 > $O/prof2_d.log 2>&1 ;;
+    asm) timeout 900 python tools/time_assembly.py > $O/assembly_${TAG}.json 2> $O/asm_d.err ;;
+  esac
+  echo "$s: $(( $(date +%s) - t0 )) s" >> $O/steps_d.txt
+done
