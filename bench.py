@@ -108,7 +108,31 @@ def file_hash(path):
     return h.hexdigest()[:12]
 
 
-def get_hierarchy(P, cfg, scale, rank, dist, threads, setup_device=None):
+def host_slots(ws, need_bytes, total_bytes=None):
+    """How many ranks may hold a host copy of the hierarchy at the same time (replicas, N > 1):
+    80 % of the host RAM over the per-rank need, at least 1, at most ws."""
+    if total_bytes is None:
+        try:
+            import psutil
+            total_bytes = psutil.virtual_memory().total
+        except Exception:
+            total_bytes = 64 << 30
+    return int(max(1, min(ws, (0.8 * total_bytes) // max(1, need_bytes))))
+
+
+def staged(dist, rank, ws, slots, fn):
+    """Run fn() on every rank, at most `slots` ranks at a time (rank order), with a barrier
+    between the turns: bounds the host memory of N replicas that each load + upload the
+    same hierarchy (C5: 36 GB per rank)."""
+    out = None
+    for turn in range(0, ws, max(1, slots)):
+        if turn <= rank < turn + max(1, slots):
+            out = fn()
+        dist.barrier()
+    return out
+
+
+def get_hierarchy(P, cfg, scale, rank, dist, threads, setup_device=None, load=True):
     """Setup once (rank 0), cached on disk for the other ranks / reruns. With
     setup_device the SRQCG, aFSAI and Galerkin phases run on that GPU (the
     identical hierarchy, tests/test_gpu_setup.py). Returns the setup's origin
@@ -136,8 +160,8 @@ def get_hierarchy(P, cfg, scale, rank, dist, threads, setup_device=None):
         os.replace(path + ".tmp", path)
     dist.barrier()
     if t_setup is None:
-        h = P.Hierarchy.load(path)
-        t_setup = h.info().T_p
+        h = P.Hierarchy.load(path) if load else path  # load=False: the caller loads (staged, N > 1)
+        t_setup = h.info().T_p if load else 0.0
         try:
             with open(path + ".json") as f:
                 origin = "cached: " + json.load(f)["origin"]
@@ -308,11 +332,30 @@ def run_b200(args, ws, rank, local):
     # setup (outside the timed region): CPU, with the SRQCG + Galerkin phases on this
     # rank's GPU — the identical hierarchy the all-CPU setup builds (tests/test_gpu_setup.py)
     prob, h, t_gen, t_setup, origin = get_hierarchy(P, args.config, args.scale, rank, dist, os.cpu_count() or 1,
-                                                    None if args.cpu_setup else local)
-    info = h.info()
-    t0 = time.perf_counter()
-    g = P.GpuVcycle(h, device=local)
-    t_upload = time.perf_counter() - t0
+                                                    None if args.cpu_setup else local, load=(ws == 1))
+
+    def load_and_upload():
+        hh = P.Hierarchy.load(h) if isinstance(h, str) else h
+        t0 = time.perf_counter()
+        gg = P.GpuVcycle(hh, device=local)
+        return hh, hh.info(), gg, time.perf_counter() - t0
+
+    if ws == 1:
+        h, info, g, t_upload = load_and_upload()
+    else:
+        # replicas: every rank needs the host hierarchy only until its upload is done; ranks take
+        # turns so that the host copies alive at once fit in RAM, then drop theirs
+        cache_dir = os.environ.get("ASPAMG_CACHE_DIR") or os.path.join(ROOT, ".cache")
+        sizes = [os.path.getsize(os.path.join(cache_dir, f)) for f in os.listdir(cache_dir)
+                 if f.startswith(f"hier_c{args.config}_s{args.scale}_") and f.endswith(".bin")]
+        need = int(1.3 * max(sizes)) if sizes else 1 << 30
+        hh, info, g, t_upload = staged(dist, rank, ws, host_slots(ws, need), load_and_upload)
+        if t_setup == 0.0:
+            t_setup = info.T_p
+        del hh
+        h = None
+        import gc
+        gc.collect()
     lib = N.gpu()
     n = prob.K.n_rows
     nbytes = 8 * n
