@@ -40,18 +40,29 @@ int orc_spmv(const orc_csr* A, const double* x, double* y) {
  * block partials summed in index order — an equally valid fixed order, used
  * only to measure how sensitive a solve's iteration count is to the dot's
  * summation order. */
+/* Elementwise vector updates are independent per entry: threading them changes no bit.
+ * (The CPU baseline of bench.py runs them, and the blocked dot below, on all host cores;
+ * the parity tests keep the sequential dot.) */
+#define ORC_PFOR _Pragma("omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1 && n > 16384)")
 static int g_dot_mode = 0;
 void orc_set_dot_mode(int m) { g_dot_mode = m; }
 
 static double dotp(int64_t n, const double* a, const double* b) {
     if (g_dot_mode == 1) {
-        double s = 0.0;
-        for (int64_t i0 = 0; i0 < n; i0 += 4096) {
-            const int64_t i1 = i0 + 4096 < n ? i0 + 4096 : n;
+        /* block partials (computed in parallel when threads > 1), summed in index order:
+         * the same bits for every thread count */
+        const int64_t nb = (n + 4095) / 4096;
+        double* part = (double*)malloc((size_t)(nb > 0 ? nb : 1) * sizeof(double));
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1 && nb > 8)
+        for (int64_t bk = 0; bk < nb; ++bk) {
+            const int64_t i0 = bk * 4096, i1 = i0 + 4096 < n ? i0 + 4096 : n;
             double t = 0.0;
             for (int64_t i = i0; i < i1; ++i) t += a[i] * b[i];
-            s += t;
+            part[bk] = t;
         }
+        double s = 0.0;
+        for (int64_t bk = 0; bk < nb; ++bk) s += part[bk];
+        free(part);
         return s;
     }
     double s = 0.0;
@@ -64,6 +75,7 @@ static void smooth_into(const orc_level* L, const double* b, const double* x, do
     const int64_t n = L->A.n_rows;
     if (x) {
         orc_spmv(&L->A, x, r);
+        ORC_PFOR
         for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
     } else {
         memcpy(r, b, (size_t)n * sizeof(double));
@@ -71,8 +83,10 @@ static void smooth_into(const orc_level* L, const double* b, const double* x, do
     orc_spmv(&L->G, r, t);
     orc_spmv(&L->Gt, t, r);
     if (x) {
+        ORC_PFOR
         for (int64_t i = 0; i < n; ++i) out[i] = x[i] + L->omega * r[i];
     } else {
+        ORC_PFOR
         for (int64_t i = 0; i < n; ++i) out[i] = L->omega * r[i];
     }
 }
@@ -115,11 +129,18 @@ static void vcycle_rec(const orc_hier* h, int64_t k, const double* y, double* z)
     const orc_level* L = &h->levels[k];
     const int64_t n = L->A.n_rows, nc = L->P.n_cols;
     double* s = z; /* s accumulates in z */
-    double* r = (double*)malloc((size_t)n * sizeof(double));
-    double* t = (double*)malloc((size_t)n * sizeof(double));
-    double* u = (double*)malloc((size_t)n * sizeof(double));
-    double* rc = (double*)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(double));
-    double* hc = (double*)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(double));
+    /* per-level workspace kept between V-cycles (a fresh 50-MB malloc per vector per
+     * cycle costs page faults that are not part of the algorithm) */
+    static double* ws[64][5];
+    static int64_t wsn[64], wsc[64];
+    if (k < 64 && (wsn[k] < n || wsc[k] < nc)) {
+        for (int j = 0; j < 5; ++j) free(ws[k][j]);
+        for (int j = 0; j < 3; ++j) ws[k][j] = (double*)malloc((size_t)n * sizeof(double));
+        for (int j = 3; j < 5; ++j) ws[k][j] = (double*)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(double));
+        wsn[k] = n;
+        wsc[k] = nc;
+    }
+    double *r = ws[k][0], *t = ws[k][1], *u = ws[k][2], *rc = ws[k][3], *hc = ws[k][4];
     /* nu1 pre-smoothing steps from s = 0 */
     for (int64_t it = 0; it < h->nu1; ++it) {
         if (it == 0) smooth_into(L, y, NULL, s, r, t);
@@ -128,18 +149,19 @@ static void vcycle_rec(const orc_hier* h, int64_t k, const double* y, double* z)
     if (h->nu1 == 0) memset(s, 0, (size_t)n * sizeof(double));
     /* r = y - A s ; r_c = P' r */
     orc_spmv(&L->A, s, r);
+    ORC_PFOR
     for (int64_t i = 0; i < n; ++i) r[i] = y[i] - r[i];
     orc_spmv(&L->Pt, r, rc);
     vcycle_rec(h, k + 1, rc, hc);
     /* s += P h_c */
     orc_spmv(&L->P, hc, t);
+    ORC_PFOR
     for (int64_t i = 0; i < n; ++i) s[i] = s[i] + t[i];
     /* nu2 post-smoothing steps from s */
     for (int64_t it = 0; it < h->nu2; ++it) {
         smooth_into(L, y, s, u, r, t);
         memcpy(s, u, (size_t)n * sizeof(double));
     }
-    free(r); free(t); free(u); free(rc); free(hc);
 }
 
 int orc_vcycle(const orc_hier* h, const double* y, double* z) {
@@ -186,6 +208,7 @@ int orc_pcg(const orc_hier* h, const double* b, const double* x0, double rel_tol
             const double pq = dotp(n, p, q);
             if (!(pq > 0.0)) { status = 2; break; }
             const double alpha = rz / pq;
+            ORC_PFOR
             for (int64_t i = 0; i < n; ++i) {
                 x[i] = x[i] + alpha * p[i];
                 r[i] = r[i] - alpha * q[i];
@@ -198,6 +221,7 @@ int orc_pcg(const orc_hier* h, const double* b, const double* x0, double rel_tol
             const double rz_new = dotp(n, r, z);
             const double beta = rz_new / rz;
             rz = rz_new;
+            ORC_PFOR
             for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
         }
     }
