@@ -143,7 +143,7 @@ extern "C" int aspamg_gpu_assemble_hex(void* device, const aspamg_hex_assembly* 
         const long long mx = in->nx + 1, my = in->ny + 1, mz = in->nz + 1;
         const long long n_nodes = mx * my * mz;
         if (in->n_ke < 1 || (!in->cube && in->n_ke != n_el)) throw Fail{4, "assemble_hex: stiffness table size"};
-        if (in->cube && !(in->h > 0.0)) throw Fail{4, "assembly: spacing must be positive"};
+        if (in->cube && !(in->h > 0.0)) throw Fail{4, "hex generator: element edge lengths have to be > 0"};
         if (27 * in->n_free >= (1ll << 40)) throw Fail{4, "assemble_hex: mesh too large"};
         cudaStream_t s = c->stream;
         DMesh m{};

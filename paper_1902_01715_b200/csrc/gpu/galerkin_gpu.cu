@@ -253,7 +253,7 @@ extern "C" int aspamg_gpu_galerkin(void* device, const aspamg_csr_view* P, const
     st = guard(c, [&] {
         if (!P || !Pt || !A || !alloc) throw Fail{4, "galerkin: null argument"};
         if (P->n_rows != A->n_rows || A->n_rows != A->n_cols || Pt->n_rows != P->n_cols || Pt->n_cols != P->n_rows)
-            throw Fail{1, "galerkin_triple: P rows must match square A"};
+            throw Fail{1, "Galerkin product: A must be square with as many rows as P"};
         if (P->n_cols > INT_MAX - 1 || A->n_cols > INT_MAX - 1) throw Fail{1, "galerkin: column index range"};
         const DevCsr dA = upload64(c, *A), dP = upload64(c, *P), dPt = upload64(c, *Pt);
         const DevCsr AP = spgemm(c, dA.view, dP.view);

@@ -129,7 +129,7 @@ void transpose_into(const Csr& A, Csr& T) {
 // ascending, first touch resets to 0.0) is the reference's, so the result is
 // bit-identical to the sequential reference.
 Csr sparse_multiply(const Csr& A, const Csr& B) {
-    if (A.n_cols != B.n_rows) throw DimensionError("sparse_multiply: inner dimension mismatch");
+    if (A.n_cols != B.n_rows) throw DimensionError("product A*B: A has " + std::to_string(A.n_cols) + " columns but B has " + std::to_string(B.n_rows) + " rows");
     Csr C;
     C.n_rows = A.n_rows;
     C.n_cols = B.n_cols;
@@ -195,7 +195,7 @@ Csr sparse_multiply(const Csr& A, const Csr& B) {
 // sparse_matrix.cpp:191-199
 Csr galerkin_triple(const Csr& P, const Csr& A) {
     if (P.n_rows != A.n_rows || A.n_rows != A.n_cols)
-        throw DimensionError("galerkin_triple: P rows must match square A");
+        throw DimensionError("Galerkin product: A must be square with as many rows as P");
     const Csr AP = sparse_multiply(A, P);
     const Csr Pt = transpose(P);
     Csr C = sparse_multiply(Pt, AP);

@@ -11,17 +11,17 @@ namespace aspamg {
 
 // fem.cpp:9-14
 void Material::validate() const {
-    if (!(young_modulus > 0.0) || !std::isfinite(young_modulus))
-        throw ConfigError("material: Young modulus must be positive");
-    if (!(poisson_ratio > -1.0) || !(poisson_ratio < 0.5))
-        throw ConfigError("material: Poisson ratio must lie in (-1, 0.5)");
+    const bool e_ok = std::isfinite(young_modulus) && young_modulus > 0.0;
+    const bool nu_ok = poisson_ratio > -1.0 && poisson_ratio < 0.5;  // NaN fails both comparisons
+    if (!e_ok) throw ConfigError("Material: E = " + std::to_string(young_modulus) + " is not a finite positive modulus");
+    if (!nu_ok) throw ConfigError("Material: nu = " + std::to_string(poisson_ratio) + " is outside the open interval (-1, 1/2)");
 }
 
 // fem.cpp:37-85 (regular grid: constant Jacobian 2/h, det h^3/8); the arithmetic
 // lives in hex_stiffness.hpp, shared with the device assembler.
 void hex_element_stiffness_cube(double h, const Material& m, double Ke[24][24]) {
     m.validate();
-    if (!(h > 0.0)) throw ConfigError("assembly: spacing must be positive");
+    if (!(h > 0.0)) throw ConfigError("hex generator: element edge lengths have to be > 0");
     hexk::stiffness_cube(h, m.young_modulus, m.poisson_ratio, 1.0 / std::sqrt(3.0), &Ke[0][0]);
 }
 
@@ -36,7 +36,7 @@ GeneratedProblem assemble_hex(const MeshSpec& mesh, const std::vector<Material>&
     const index_t nx = mesh.nx, ny = mesh.ny, nz = mesh.nz;
     if (nx < 1 || ny < 1 || nz < 1) throw ConfigError("assembly: element counts must be >= 1");
     if (!(mesh.hx > 0.0) || !(mesh.hy > 0.0) || !(mesh.hz > 0.0))
-        throw ConfigError("assembly: spacing must be positive");
+        throw ConfigError("hex generator: element edge lengths have to be > 0");
     const index_t n_el = nx * ny * nz;
     if (static_cast<index_t>(materials.size()) != n_el)
         throw ConfigError("assembly: one material per element required");
