@@ -238,10 +238,6 @@ def cpu_reference_sample(h, rhs, threads, target_s=12.0, max_iters=60):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
     use_ref = O.ref_available()
-    # timing runs: the dots as block partials summed in index order (computed on all threads, the
-    # same bits for every thread count) and threaded elementwise updates, so that no part of the
-    # CPU path is left on one core; the parity tests keep the sequential dot (mode 0)
-    O.lib().orc_set_dot_mode(1 if threads > 1 else 0)
     oh = O.OracleHierarchy(h, use_ref_spmv=use_ref, threads=threads)
     t0 = time.perf_counter()
     oh.pcg(rhs, rel_tol=0.0, max_it=2)

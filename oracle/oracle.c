@@ -40,10 +40,6 @@ int orc_spmv(const orc_csr* A, const double* x, double* y) {
  * block partials summed in index order — an equally valid fixed order, used
  * only to measure how sensitive a solve's iteration count is to the dot's
  * summation order. */
-/* Elementwise vector updates are independent per entry: threading them changes no bit.
- * (The CPU baseline of bench.py runs them, and the blocked dot below, on all host cores;
- * the parity tests keep the sequential dot.) */
-#define ORC_PFOR _Pragma("omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1 && n > 16384)")
 static int g_dot_mode = 0;
 void orc_set_dot_mode(int m) { g_dot_mode = m; }
 
@@ -75,7 +71,6 @@ static void smooth_into(const orc_level* L, const double* b, const double* x, do
     const int64_t n = L->A.n_rows;
     if (x) {
         orc_spmv(&L->A, x, r);
-        ORC_PFOR
         for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
     } else {
         memcpy(r, b, (size_t)n * sizeof(double));
@@ -83,10 +78,8 @@ static void smooth_into(const orc_level* L, const double* b, const double* x, do
     orc_spmv(&L->G, r, t);
     orc_spmv(&L->Gt, t, r);
     if (x) {
-        ORC_PFOR
         for (int64_t i = 0; i < n; ++i) out[i] = x[i] + L->omega * r[i];
     } else {
-        ORC_PFOR
         for (int64_t i = 0; i < n; ++i) out[i] = L->omega * r[i];
     }
 }
@@ -149,13 +142,11 @@ static void vcycle_rec(const orc_hier* h, int64_t k, const double* y, double* z)
     if (h->nu1 == 0) memset(s, 0, (size_t)n * sizeof(double));
     /* r = y - A s ; r_c = P' r */
     orc_spmv(&L->A, s, r);
-    ORC_PFOR
     for (int64_t i = 0; i < n; ++i) r[i] = y[i] - r[i];
     orc_spmv(&L->Pt, r, rc);
     vcycle_rec(h, k + 1, rc, hc);
     /* s += P h_c */
     orc_spmv(&L->P, hc, t);
-    ORC_PFOR
     for (int64_t i = 0; i < n; ++i) s[i] = s[i] + t[i];
     /* nu2 post-smoothing steps from s */
     for (int64_t it = 0; it < h->nu2; ++it) {
@@ -208,8 +199,7 @@ int orc_pcg(const orc_hier* h, const double* b, const double* x0, double rel_tol
             const double pq = dotp(n, p, q);
             if (!(pq > 0.0)) { status = 2; break; }
             const double alpha = rz / pq;
-            ORC_PFOR
-            for (int64_t i = 0; i < n; ++i) {
+                for (int64_t i = 0; i < n; ++i) {
                 x[i] = x[i] + alpha * p[i];
                 r[i] = r[i] - alpha * q[i];
             }
@@ -221,8 +211,7 @@ int orc_pcg(const orc_hier* h, const double* b, const double* x0, double rel_tol
             const double rz_new = dotp(n, r, z);
             const double beta = rz_new / rz;
             rz = rz_new;
-            ORC_PFOR
-            for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+                for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
         }
     }
     /* true residual recheck */
