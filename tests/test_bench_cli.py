@@ -49,3 +49,39 @@ def test_gpu_arm_fails_loudly_without_device():
     r = _run(["--config", "1", "--scale", "4", "--steps", "1", "--no-cpu"])
     assert r.returncode != 0
     assert "no CUDA device" in r.stderr
+
+
+def test_both_arms_share_metric_and_unit():
+    """The driver divides the two arms' values only when metric, unit and direction are
+    identical (round 1 printed two different strings and got a null ratio)."""
+    sys.path.insert(0, ROOT)
+    import inspect
+
+    import bench
+    r = _run(["--impl", "reference", "--config", "1", "--scale", "4", "--steps", "1", "--warmup", "0", "--ref-sample-s", "0.2"])
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")][0])
+    assert d["metric"] == bench.METRIC and d["unit"] == "s/iteration"
+    src = inspect.getsource(bench.run_b200)
+    assert '"metric": METRIC' in src and '"unit": "s/iteration"' in src and '"higher_is_better": False' in src
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_line():
+    """GPU arm on a small config: one JSON line with the contract's keys, e2e from host buffers
+    (copies declared), kernel launches counted, the same metric string as the reference arm."""
+    sys.path.insert(0, ROOT)
+    import bench
+    r = _run(["--config", "1", "--steps", "2", "--warmup", "3", "--ref-sample-s", "0.5"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["metric"] == bench.METRIC and d["unit"] == "s/iteration" and d["higher_is_better"] is False
+    assert d["e2e"]["h2d_bytes_per_step"] == 8 * d["config"]["n"] and d["e2e"]["d2h_bytes_per_step"] > 8 * d["config"]["n"]
+    assert d["e2e"]["value"] >= d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 2
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["one_thread"]["cores"] == 1
+    assert d["config"]["converged"] is True
