@@ -117,3 +117,30 @@ def test_xsell_layout_walk_is_bit_exact(pkg, rows, fold, gran):
     A.eliminate_zeros()
     A.sort_indices()
     check(pkg.SparseMatrix.from_scipy(A))
+
+
+def test_view_validation_without_a_device(pkg):
+    """check_view (context.cu) through the host-only layout entry point: sizes past the int32
+    device indexing are a ConfigError (status 4) before any array is scanned; malformed views
+    (nnz mismatch, column out of range, unsorted row) are DimensionErrors (status 1)."""
+    import numpy as np
+    from paper_1902_01715_b200 import _native as N
+    lib = N.gpu()
+    P_d = C.POINTER(C.c_double)
+    x = np.zeros(4)
+    y = np.zeros(4)
+
+    def status(n_rows, n_cols, nnz, rp, ci, va):
+        rp = np.asarray(rp, np.int64)
+        ci = np.asarray(ci, np.int64)
+        va = np.asarray(va, np.float64)
+        v = N.CsrView(n_rows, n_cols, nnz, rp.ctypes.data_as(C.POINTER(C.c_int64)),
+                      ci.ctypes.data_as(C.POINTER(C.c_int64)), va.ctypes.data_as(P_d))
+        return lib.aspamg_gpu_xsell_layout_spmv(C.byref(v), 32, 1, 1, x.ctypes.data_as(P_d), y.ctypes.data_as(P_d))
+
+    big = 1 << 31
+    assert status(1, 4, big, [0, big], [0], [1.0]) == 4          # nnz >= 2^31: exceeds device indexing
+    assert status(2, 4, 3, [0, 2, 2], [0, 1], [1.0, 1.0]) == 1    # row_offsets[n] != nnz
+    assert status(2, 4, 2, [0, 1, 2], [0, 7], [1.0, 1.0]) == 1    # column out of range
+    assert status(1, 4, 2, [0, 2], [2, 1], [1.0, 1.0]) == 1       # columns not ascending
+    assert status(2, 4, 2, [0, 1, 2], [0, 3], [1.0, 1.0]) == 0    # well-formed
